@@ -1,0 +1,141 @@
+"""ctypes wrapper around oracle/liboracle.so (TEST INFRASTRUCTURE ONLY).
+
+Argument marshalling only; every number is computed in ``oracle.cpp``.
+Arrays use the ABI layout ``[5][nz][ny][nx]`` (x fastest), fp64.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+import subprocess
+from dataclasses import dataclass
+from fractions import Fraction
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.cpp")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so with strict IEEE evaluation (no FMA contraction)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(
+            ["g++", "-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c++17",
+             "-shared", "-fPIC", _SRC, "-o", tmp])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+class _CParams(ctypes.Structure):
+    _fields_ = [("nx", ctypes.c_int), ("ny", ctypes.c_int), ("nz", ctypes.c_int),
+                ("order", ctypes.c_int), ("dx", ctypes.c_double), ("dt", ctypes.c_double),
+                ("Re", ctypes.c_double), ("Pr", ctypes.c_double), ("Minf", ctypes.c_double),
+                ("gamma", ctypes.c_double)]
+
+
+@dataclass
+class OracleParams:
+    nx: int
+    ny: int
+    nz: int
+    order: int
+    dx: float
+    dt: float = 0.0
+    Re: float = 1600.0
+    Pr: float = 0.71
+    Minf: float = 0.1
+    gamma: float = 1.4
+
+    def c(self) -> _CParams:
+        return _CParams(self.nx, self.ny, self.nz, self.order, self.dx, self.dt,
+                        self.Re, self.Pr, self.Minf, self.gamma)
+
+    @property
+    def shape(self):
+        return (5, self.nz, self.ny, self.nx)
+
+
+def _L():
+    global _lib
+    if _lib is None:
+        _lib = ctypes.CDLL(build())
+        P = ctypes.POINTER(_CParams)
+        dp = ctypes.POINTER(ctypes.c_double)
+        llp = ctypes.POINTER(ctypes.c_longlong)
+        _lib.oracle_weights_exact.argtypes = [ctypes.c_int, llp, llp, llp, llp]
+        _lib.oracle_derivative.argtypes = [P, dp, ctypes.c_int, ctypes.c_int, ctypes.c_int, dp]
+        _lib.oracle_residual.argtypes = [P, dp, dp]
+        _lib.oracle_step.argtypes = [P, dp, ctypes.c_int, ctypes.c_int]
+        _lib.oracle_diagnostics.argtypes = [P, dp, dp]
+        _lib.oracle_run_series.argtypes = [P, dp, ctypes.c_int, ctypes.c_int, dp]
+    return _lib
+
+
+def _dp(a: np.ndarray):
+    assert a.dtype == np.float64 and a.flags["C_CONTIGUOUS"]
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def weights_exact(order: int):
+    """(a_1..a_m, b_0..b_m) as Fractions, solved exactly from the moment conditions."""
+    m = order // 2
+    an = (ctypes.c_longlong * max(m, 1))()
+    ad = (ctypes.c_longlong * max(m, 1))()
+    bn = (ctypes.c_longlong * (m + 1))()
+    bd = (ctypes.c_longlong * (m + 1))()
+    if _L().oracle_weights_exact(order, an, ad, bn, bd) != 0:
+        raise ValueError(f"invalid order {order}")
+    return ([Fraction(an[k], ad[k]) for k in range(m)],
+            [Fraction(bn[k], bd[k]) for k in range(m + 1)])
+
+
+def derivative(p: OracleParams, f: np.ndarray, kind: int, direction: int, direction2: int = 0):
+    """kind 1: D_dir f, 2: D_dir,dir f, 3: D_dir(D_dir2 f).  f is [nz][ny][nx]."""
+    f = np.ascontiguousarray(f, dtype=np.float64)
+    out = np.empty_like(f)
+    if _L().oracle_derivative(ctypes.byref(p.c()), _dp(f), kind, direction, direction2, _dp(out)):
+        raise ValueError("bad derivative arguments")
+    return out
+
+
+def residual(p: OracleParams, Q: np.ndarray) -> np.ndarray:
+    Q = np.ascontiguousarray(Q, dtype=np.float64).reshape(p.shape)
+    R = np.empty_like(Q)
+    if _L().oracle_residual(ctypes.byref(p.c()), _dp(Q), _dp(R)):
+        raise ValueError("bad residual arguments")
+    return R
+
+
+def step(p: OracleParams, Q: np.ndarray, scheme: int, nsteps: int) -> np.ndarray:
+    """Return Q advanced by nsteps (scheme 0 = Euler, 1 = RK3); input untouched."""
+    Qn = np.array(Q, dtype=np.float64, order="C").reshape(p.shape).copy()
+    if _L().oracle_step(ctypes.byref(p.c()), _dp(Qn), scheme, nsteps):
+        raise ValueError("bad step arguments")
+    return Qn
+
+
+def diagnostics(p: OracleParams, Q: np.ndarray):
+    """(E_k, enstrophy, dissipation) — means over the grid points."""
+    Q = np.ascontiguousarray(Q, dtype=np.float64).reshape(p.shape)
+    out = np.zeros(3)
+    if _L().oracle_diagnostics(ctypes.byref(p.c()), _dp(Q), _dp(out)):
+        raise ValueError("bad diagnostics arguments")
+    return tuple(float(v) for v in out)
+
+
+def run_series(p: OracleParams, Q: np.ndarray, scheme: int, nsteps: int):
+    """Diagnostics at steps 0..nsteps -> array [nsteps+1, 3]; returns (series, Q_final)."""
+    Qn = np.array(Q, dtype=np.float64, order="C").reshape(p.shape).copy()
+    series = np.zeros((nsteps + 1, 3))
+    if _L().oracle_run_series(ctypes.byref(p.c()), _dp(Qn), scheme, nsteps, _dp(series)):
+        raise ValueError("bad run_series arguments")
+    return series, Qn
+
+
+def is_inviscid(Re: float) -> bool:
+    return math.isinf(Re)
