@@ -1,0 +1,136 @@
+/*
+ * osbli.h — C ABI of the B200-native OpenSBLI hot path (libosbli.so).
+ *
+ * The operation behind this boundary is the explicit time integration of the
+ * 3D compressible Navier-Stokes equations of Jacobs, Jammy & Sandham,
+ * "OpenSBLI ..." (arXiv 1609.01277), as the paper's generated solver performs
+ * it (PAPER.md; "P:n" = line n):
+ *   - equations (5)-(9): mass, momentum, energy, stress tensor
+ *     tau_ij, heat flux q_j, non-dimensional, constant viscosity (mu = 1);
+ *   - equation of state and total energy (10)-(11), P:259-266;
+ *   - skew-symmetric convective terms (12), with phi = 1, u_i, E;
+ *     viscous Laplacians by second-derivative stencils, P:274;
+ *     nested derivatives evaluated inner first, P:98;
+ *   - central differences of arbitrary even order, P:123;
+ *   - forward Euler or the 3-stage low-storage RK3, P:123 and P:164;
+ *   - periodic boundaries in every direction, P:141 and P:276;
+ *   - volume-averaged kinetic energy and enstrophy, plus the viscous
+ *     dissipation rate (reading D-12).
+ * DESIGN.md §3 lists every reading of a point the paper leaves open.
+ *
+ * Layout of every state array crossing this boundary: fp64, [5][nz][ny][nx],
+ * x fastest; field order (rho, rho*u, rho*v, rho*w, rho*E).  In distributed mode
+ * nz is this rank's slab (osbli_local_box).  Grid point (i,j,k) sits at
+ * (i*dx, j*dx, k*dx); the periodic box is nx*dx x ny*dx x (global nz)*dx.
+ *
+ * Ownership: the library owns all device memory it allocates (state ping-pong
+ * buffers, RK register, scratch, NCCL communicator).  Caller pointers are only
+ * read or written during the call and never retained.  Device pointers must be
+ * on the handle's device.
+ *
+ * Synchronisation: osbli_step only enqueues work on the handle's stream and
+ * returns; set_state/get_state/diagnostics/residual/sync complete before they
+ * return.  A non-finite value produced by a step is reported (OSBLI_E_NONFINITE)
+ * by the next synchronising call.
+ *
+ * Errors: every int-returning call returns OSBLI_OK (0) or a negative status;
+ * no exception or abort crosses the ABI.  After OSBLI_E_CUDA, OSBLI_E_COMM or
+ * OSBLI_E_NONFINITE the handle is poisoned: only get_state, last_error and
+ * destroy remain valid (others return OSBLI_E_STATE).
+ */
+#ifndef OSBLI_H
+#define OSBLI_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct osbli_ctx osbli_ctx;
+
+/* Time schemes: forward Euler, and the 3-stage 2N-storage RK3
+ * (Williamson coefficients in Carpenter-Kennedy 2N form; D-1). */
+enum { OSBLI_EULER = 0, OSBLI_RK3 = 1 };
+
+enum {
+  OSBLI_OK = 0,
+  OSBLI_E_INVAL = -1,       /* invalid argument                                  */
+  OSBLI_E_UNSUPPORTED = -2, /* valid but not built (order > 12)                  */
+  OSBLI_E_NOMEM = -3,       /* device allocation failed                          */
+  OSBLI_E_CUDA = -4,        /* CUDA runtime error (text in osbli_last_error)     */
+  OSBLI_E_COMM = -5,        /* NCCL error                                        */
+  OSBLI_E_NONFINITE = -6,   /* a step produced NaN/Inf                           */
+  OSBLI_E_STATE = -7        /* handle poisoned by an earlier error               */
+};
+
+/* Diagnostics at the current time t = step*dt (D-11/D-12):
+ * means over all grid points (rectangle rule on the periodic box, rho_ref = 1):
+ *   kinetic_energy = <1/2 rho u_j u_j>, enstrophy = <1/2 rho |curl u|^2>,
+ *   dissipation    = <tau_ij du_i/dx_j>, derivatives by the solver's stencils. */
+typedef struct {
+  double t;
+  long long step;
+  double kinetic_energy, enstrophy, dissipation;
+} osbli_diag;
+
+/* Create a single-GPU solver on the current CUDA device.
+ *   nx,ny,nz >= 1 grid points; order even, 2..12 (else INVAL / UNSUPPORTED);
+ *   dx > 0 isotropic spacing; dt > 0 time step;
+ *   Re > 0 (Re = +INFINITY means inviscid: nu = kappa = 0); Pr > 0; Minf > 0;
+ *   gamma > 1; scheme OSBLI_EULER or OSBLI_RK3.
+ * The state is zero until osbli_set_state.  *out receives the handle. */
+int osbli_create(int nx, int ny, int nz, int order, double dx, double dt, double Re, double Pr,
+                 double Minf, double gamma, int scheme, osbli_ctx **out);
+
+/* Create one rank of a z-slab decomposition over nranks GPUs (one process per
+ * GPU).  nz is the GLOBAL size; rank r owns a contiguous slab of near-equal
+ * size (osbli_local_box), each at least order/2 planes.  nccl_unique_id points
+ * to the 128-byte ncclUniqueId produced by osbli_nccl_unique_id on rank 0 and
+ * broadcast by the caller.  The CUDA device must be set by the caller. */
+int osbli_create_dist(int nx, int ny, int nz, int order, double dx, double dt, double Re,
+                      double Pr, double Minf, double gamma, int scheme, int rank, int nranks,
+                      const void *nccl_unique_id, osbli_ctx **out);
+
+/* Fill 128 bytes at id_out with a fresh ncclUniqueId (rank 0 only). */
+int osbli_nccl_unique_id(void *id_out);
+
+/* Slab owned by this rank: global planes [*z0, *z0 + *nz_local). */
+int osbli_local_box(const osbli_ctx *h, int *z0, int *nz_local);
+
+/* Use this CUDA stream (cudaStream_t, e.g. torch.cuda.current_stream().cuda_stream)
+ * for all subsequent work; NULL selects the library's own stream. */
+int osbli_set_stream(osbli_ctx *h, void *cuda_stream);
+
+/* Copy the conservative state in / out.  q is [5][nz_local][ny][nx] fp64, on the
+ * host (on_device = 0) or on the handle's device (on_device = 1).  set_state
+ * resets the RK register and the step counter. */
+int osbli_set_state(osbli_ctx *h, const double *q, int on_device);
+int osbli_get_state(osbli_ctx *h, double *q, int on_device);
+
+/* Advance n >= 0 full time steps (3 stages for RK3).  Stream-ordered. */
+int osbli_step(osbli_ctx *h, int n);
+
+/* Diagnostics of the current state (collective over ranks when distributed:
+ * every rank gets the same, decomposition-independent numbers). */
+int osbli_diagnostics(osbli_ctx *h, osbli_diag *out);
+
+/* Test hook: R(Q) of the current state, [5][nz_local][ny][nx], no update. */
+int osbli_residual(osbli_ctx *h, double *R, int on_device);
+
+/* Wait for queued work; surfaces asynchronous errors (NONFINITE, CUDA). */
+int osbli_sync(osbli_ctx *h);
+
+/* Number of kernels this handle launched since creation (instrumentation). */
+long long osbli_kernel_launches(const osbli_ctx *h);
+
+/* Last error text for h; h == NULL gives the calling thread's last create error. */
+const char *osbli_last_error(const osbli_ctx *h);
+
+/* Library build string: "osbli <version> sm_100a orders 2..12". */
+const char *osbli_version(void);
+
+void osbli_destroy(osbli_ctx *h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OSBLI_H */

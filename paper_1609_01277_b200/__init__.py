@@ -1,0 +1,22 @@
+"""B200-native OpenSBLI hot path: thin Python binding over libosbli.so (C ABI).
+
+Every step of the path runs in the library's sm_100a kernels; this module only
+marshals arguments (ctypes).  There is no CPU fallback: importing the binding
+without a built ``libosbli.so`` raises immediately, and any call on a machine
+without a CUDA device fails with the library's CUDA error.
+
+PyTorch is used only for device memory and streams (torch tensors are passed
+as device pointers) and process groups (``init_distributed``).
+"""
+from .native import (  # noqa: F401
+    OSBLI_EULER,
+    OSBLI_RK3,
+    OsbliError,
+    Solver,
+    build,
+    lib_path,
+    load,
+    nccl_unique_id,
+    version,
+)
+from .distributed import init_distributed, slab_bounds  # noqa: F401

@@ -1,0 +1,495 @@
+// =============================================================================
+// C ABI + runtime of the B200-native OpenSBLI hot path (see include/osbli.h).
+//
+// Owns the device buffers of one handle, sequences the stages of the time
+// scheme, exchanges z ghost planes between ranks over NCCL
+// (slab decomposition) and reduces the diagnostics
+// deterministically (per-plane partials summed in global plane order).
+// =============================================================================
+#include "../../include/osbli.h"
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "kernels.h"
+
+using osbli::Bufs;
+using osbli::KParams;
+
+struct osbli_ctx {
+  int nx = 0, ny = 0, nz_global = 0, nz = 0, z0 = 0, order = 0, m = 0, scheme = 0;
+  int rank = 0, nranks = 1;
+  double dx = 0, dt = 0, Re = 0, Pr = 0, Minf = 0, gamma = 0;
+  int device = 0;
+  cudaStream_t stream = nullptr, own_stream = nullptr;
+  Bufs b{};
+  double *scratch = nullptr;  // velocity for diagnostics, [nz + 2G][3][ny][nx]
+  double *nccl_part = nullptr;  // [nranks * max_nz][3] gathered plane partials
+  int max_nz = 0;
+  int cur = 0;
+  long long step_count = 0;
+  long long launches = 0;
+  bool poisoned = false;
+  std::string err;
+  ncclComm_t comm = nullptr;
+  KParams base{};
+};
+
+namespace {
+
+thread_local std::string g_create_error;
+
+struct Frac64 {
+  long long n, d;
+};
+
+long long gcdll(long long a, long long b) {
+  if (a < 0) a = -a;
+  if (b < 0) b = -b;
+  while (b) {
+    long long t = a % b;
+    a = b;
+    b = t;
+  }
+  return a;
+}
+
+long long fact(int n) {
+  long long r = 1;
+  for (int i = 2; i <= n; ++i) r *= i;
+  return r;
+}
+
+// Central-difference weights in closed form (explicit Lagrange-derivative
+// formula; exact in int64 for m <= 6):
+//   a_k = (-1)^(k+1) (m!)^2 / (k (m-k)! (m+k)!)
+//   b_k = 2 (-1)^(k+1) (m!)^2 / (k^2 (m-k)! (m+k)!),  b_0 = -2 sum_k b_k
+void weights(int m, double *a, double *b) {
+  const long long mf2 = fact(m) * fact(m);
+  std::vector<Frac64> bk;
+  for (int k = 1; k <= m; ++k) {
+    const long long sgn = (k % 2 == 1) ? 1 : -1;
+    long long n = sgn * mf2, d = (long long)k * fact(m - k) * fact(m + k);
+    long long g = gcdll(n, d);
+    a[k - 1] = (double)(n / g) / (double)(d / g);
+    long long n2 = 2 * sgn * mf2, d2 = (long long)k * k * fact(m - k) * fact(m + k);
+    g = gcdll(n2, d2);
+    bk.push_back({n2 / g, d2 / g});
+    b[k] = (double)(n2 / g) / (double)(d2 / g);
+  }
+  // b_0 exactly: sum of fractions
+  long long N = 0, D = 1;
+  for (auto &f : bk) {
+    const long long g = gcdll(D, f.d);
+    const long long L = D / g * f.d;
+    N = N * (L / D) + f.n * (L / f.d);
+    D = L;
+    const long long h = gcdll(N, D);
+    if (h > 1) { N /= h; D /= h; }
+  }
+  b[0] = -2.0 * (double)N / (double)D;
+}
+
+int fail(osbli_ctx *h, int code, const std::string &msg) {
+  h->err = msg;
+  if (code == OSBLI_E_CUDA || code == OSBLI_E_COMM || code == OSBLI_E_NONFINITE) h->poisoned = true;
+  return code;
+}
+
+int cuda_fail(osbli_ctx *h, cudaError_t e, const char *where) {
+  return fail(h, OSBLI_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(h, expr)                                          \
+  do {                                                       \
+    cudaError_t _e = (expr);                                 \
+    if (_e != cudaSuccess) return cuda_fail((h), _e, #expr); \
+  } while (0)
+
+#define NK(h, expr)                                                                 \
+  do {                                                                              \
+    ncclResult_t _r = (expr);                                                       \
+    if (_r != ncclSuccess)                                                          \
+      return fail((h), OSBLI_E_COMM, std::string(#expr) + ": " + ncclGetErrorString(_r)); \
+  } while (0)
+
+int validate(int nx, int ny, int nz, int order, double dx, double dt, double Re, double Pr,
+             double Minf, double gamma, int scheme, std::string &msg) {
+  if (nx < 1 || ny < 1 || nz < 1) { msg = "grid sizes must be >= 1"; return OSBLI_E_INVAL; }
+  if (order < 2 || order % 2 != 0) { msg = "order must be even and >= 2"; return OSBLI_E_INVAL; }
+  if (!(dx > 0.0) || !std::isfinite(dx)) { msg = "dx must be finite and > 0"; return OSBLI_E_INVAL; }
+  if (!(dt > 0.0) || !std::isfinite(dt)) { msg = "dt must be finite and > 0"; return OSBLI_E_INVAL; }
+  if (!(Re > 0.0)) { msg = "Re must be > 0 (or +inf)"; return OSBLI_E_INVAL; }
+  if (!(Pr > 0.0) || !std::isfinite(Pr)) { msg = "Pr must be > 0"; return OSBLI_E_INVAL; }
+  if (!(Minf > 0.0) || !std::isfinite(Minf)) { msg = "Minf must be > 0"; return OSBLI_E_INVAL; }
+  if (!(gamma > 1.0) || !std::isfinite(gamma)) { msg = "gamma must be > 1"; return OSBLI_E_INVAL; }
+  if (scheme != OSBLI_EULER && scheme != OSBLI_RK3) { msg = "scheme must be 0 or 1"; return OSBLI_E_INVAL; }
+  if (order > 2 * osbli::kMaxHalf) { msg = "orders above 12 are not built"; return OSBLI_E_UNSUPPORTED; }
+  return OSBLI_OK;
+}
+
+void free_all(osbli_ctx *h) {
+  cudaFree(h->b.q[0]);
+  cudaFree(h->b.q[1]);
+  cudaFree(h->b.w);
+  cudaFree(h->b.rz);
+  cudaFree(h->b.gz);
+  cudaFree(h->b.flag);
+  cudaFree(h->b.diag_part);
+  cudaFree(h->scratch);
+  cudaFree(h->nccl_part);
+  h->b = Bufs{};
+  h->scratch = nullptr;
+  h->nccl_part = nullptr;
+}
+
+int create_common(osbli_ctx *h) {
+  CK(h, cudaGetDevice(&h->device));
+  h->m = h->order / 2;
+  const int G = h->m;
+  const size_t FS = (size_t)h->nx * h->ny;
+  const size_t qn = (size_t)(h->nz + 2 * G) * 5 * FS;
+  auto alloc = [&](double **p, size_t n) -> cudaError_t {
+    return cudaMalloc((void **)p, n * sizeof(double));
+  };
+  cudaError_t e = cudaSuccess;
+  if ((e = alloc(&h->b.q[0], qn)) != cudaSuccess || (e = alloc(&h->b.q[1], qn)) != cudaSuccess ||
+      (e = alloc(&h->b.w, (size_t)h->nz * 5 * FS)) != cudaSuccess ||
+      (e = alloc(&h->b.rz, (size_t)h->nz * 5 * FS)) != cudaSuccess ||
+      (e = alloc(&h->b.gz, (size_t)h->nz * 3 * FS)) != cudaSuccess ||
+      (e = alloc(&h->scratch, (size_t)(h->nz + 2 * G) * 3 * FS)) != cudaSuccess ||
+      (e = alloc(&h->b.diag_part, (size_t)3 * h->nz)) != cudaSuccess ||
+      (e = cudaMalloc((void **)&h->b.flag, sizeof(unsigned int))) != cudaSuccess) {
+    free_all(h);
+    cudaGetLastError();
+    h->err = std::string("device allocation failed: ") + cudaGetErrorString(e);
+    return OSBLI_E_NOMEM;
+  }
+  CK(h, cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking));
+  h->stream = h->own_stream;
+  CK(h, cudaMemsetAsync(h->b.q[0], 0, qn * sizeof(double), h->stream));
+  CK(h, cudaMemsetAsync(h->b.q[1], 0, qn * sizeof(double), h->stream));
+  CK(h, cudaMemsetAsync(h->b.w, 0, (size_t)h->nz * 5 * FS * sizeof(double), h->stream));
+  CK(h, cudaMemsetAsync(h->b.flag, 0, sizeof(unsigned int), h->stream));
+
+  KParams &p = h->base;
+  p = KParams{};
+  p.nx = h->nx;
+  p.ny = h->ny;
+  p.nz = h->nz;
+  p.G = G;
+  p.zwrap = (h->nranks == 1) ? 1 : 0;
+  p.m = h->m;
+  double a[osbli::kMaxHalf] = {0}, b[osbli::kMaxHalf + 1] = {0};
+  weights(h->m, a, b);
+  for (int k = 0; k < h->m; ++k) p.a[k] = a[k] / h->dx;
+  for (int k = 0; k <= h->m; ++k) p.b[k] = b[k] / (h->dx * h->dx);
+  const bool inviscid = std::isinf(h->Re);
+  p.nu = inviscid ? 0.0 : 1.0 / h->Re;
+  p.kappa = inviscid ? 0.0 : 1.0 / ((h->gamma - 1.0) * h->Minf * h->Minf * h->Pr * h->Re);
+  p.gm1 = h->gamma - 1.0;
+  p.gM2 = h->gamma * h->Minf * h->Minf;
+  p.dt = h->dt;
+  CK(h, cudaStreamSynchronize(h->stream));
+  return OSBLI_OK;
+}
+
+int check_usable(osbli_ctx *h) {
+  if (!h) return OSBLI_E_INVAL;
+  if (h->poisoned) return OSBLI_E_STATE;
+  return OSBLI_OK;
+}
+
+// z ghost planes of Q buffer `q` from the neighbouring slabs (periodic ring).
+int exchange_ghosts(osbli_ctx *h, double *q) {
+  if (h->nranks == 1) return OSBLI_OK;
+  const int G = h->m;
+  const size_t FS = (size_t)h->nx * h->ny;
+  const size_t cnt = (size_t)G * 5 * FS;
+  const size_t plane = 5 * FS;
+  const int up = (h->rank + 1) % h->nranks, dn = (h->rank - 1 + h->nranks) % h->nranks;
+  double *interior_lo = q + (size_t)G * plane;          // planes [0, G)
+  double *interior_hi = q + (size_t)h->nz * plane;      // planes [nz-G, nz)
+  double *ghost_lo = q;                                 // planes [-G, 0)
+  double *ghost_hi = q + (size_t)(h->nz + G) * plane;   // planes [nz, nz+G)
+  NK(h, ncclGroupStart());
+  NK(h, ncclSend(interior_lo, cnt, ncclDouble, dn, h->comm, h->stream));
+  NK(h, ncclRecv(ghost_hi, cnt, ncclDouble, up, h->comm, h->stream));
+  NK(h, ncclSend(interior_hi, cnt, ncclDouble, up, h->comm, h->stream));
+  NK(h, ncclRecv(ghost_lo, cnt, ncclDouble, dn, h->comm, h->stream));
+  NK(h, ncclGroupEnd());
+  return OSBLI_OK;
+}
+
+int check_flag(osbli_ctx *h) {
+  unsigned int flag = 0;
+  CK(h, cudaMemcpyAsync(&flag, h->b.flag, sizeof(flag), cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  if (flag) return fail(h, OSBLI_E_NONFINITE, "a time step produced a non-finite value");
+  return OSBLI_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *osbli_version(void) { return "osbli 0.1 sm_100a fp64 orders 2..12"; }
+
+int osbli_create(int nx, int ny, int nz, int order, double dx, double dt, double Re, double Pr,
+                 double Minf, double gamma, int scheme, osbli_ctx **out) {
+  if (!out) return OSBLI_E_INVAL;
+  *out = nullptr;
+  std::string msg;
+  int v = validate(nx, ny, nz, order, dx, dt, Re, Pr, Minf, gamma, scheme, msg);
+  if (v != OSBLI_OK) { g_create_error = msg; return v; }
+  osbli_ctx *h = new (std::nothrow) osbli_ctx();
+  if (!h) return OSBLI_E_NOMEM;
+  h->nx = nx; h->ny = ny; h->nz_global = nz; h->nz = nz; h->z0 = 0;
+  h->order = order; h->scheme = scheme;
+  h->dx = dx; h->dt = dt; h->Re = Re; h->Pr = Pr; h->Minf = Minf; h->gamma = gamma;
+  int r = create_common(h);
+  if (r != OSBLI_OK) {
+    g_create_error = h->err;
+    free_all(h);
+    if (h->own_stream) cudaStreamDestroy(h->own_stream);
+    delete h;
+    return r;
+  }
+  *out = h;
+  return OSBLI_OK;
+}
+
+int osbli_nccl_unique_id(void *id_out) {
+  if (!id_out) return OSBLI_E_INVAL;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) { g_create_error = "ncclGetUniqueId failed"; return OSBLI_E_COMM; }
+  std::memcpy(id_out, &id, sizeof(id));
+  return OSBLI_OK;
+}
+
+int osbli_create_dist(int nx, int ny, int nz, int order, double dx, double dt, double Re,
+                      double Pr, double Minf, double gamma, int scheme, int rank, int nranks,
+                      const void *nccl_unique_id, osbli_ctx **out) {
+  if (!out) return OSBLI_E_INVAL;
+  *out = nullptr;
+  std::string msg;
+  int v = validate(nx, ny, nz, order, dx, dt, Re, Pr, Minf, gamma, scheme, msg);
+  if (v != OSBLI_OK) { g_create_error = msg; return v; }
+  if (nranks < 1 || rank < 0 || rank >= nranks || (nranks > 1 && !nccl_unique_id)) {
+    g_create_error = "bad rank / nranks / unique id";
+    return OSBLI_E_INVAL;
+  }
+  const int m = order / 2;
+  // near-equal slabs: the first (nz % nranks) ranks get one extra plane
+  const int base = nz / nranks, extra = nz % nranks;
+  const int nzl = base + (rank < extra ? 1 : 0);
+  const int z0 = rank * base + (rank < extra ? rank : extra);
+  if (nranks > 1 && base < m) {
+    g_create_error = "every slab needs at least order/2 planes";
+    return OSBLI_E_INVAL;
+  }
+  osbli_ctx *h = new (std::nothrow) osbli_ctx();
+  if (!h) return OSBLI_E_NOMEM;
+  h->nx = nx; h->ny = ny; h->nz_global = nz; h->nz = nzl; h->z0 = z0;
+  h->order = order; h->scheme = scheme; h->rank = rank; h->nranks = nranks;
+  h->max_nz = base + (extra ? 1 : 0);
+  h->dx = dx; h->dt = dt; h->Re = Re; h->Pr = Pr; h->Minf = Minf; h->gamma = gamma;
+  int r = create_common(h);
+  if (r == OSBLI_OK && nranks > 1) {
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_unique_id, sizeof(id));
+    ncclResult_t nr = ncclCommInitRank(&h->comm, nranks, id, rank);
+    if (nr != ncclSuccess) {
+      h->err = std::string("ncclCommInitRank: ") + ncclGetErrorString(nr);
+      r = OSBLI_E_COMM;
+    } else if (cudaMalloc((void **)&h->nccl_part, (size_t)3 * nranks * h->max_nz * sizeof(double)) !=
+               cudaSuccess) {
+      h->err = "device allocation failed";
+      r = OSBLI_E_NOMEM;
+    }
+  }
+  if (r != OSBLI_OK) {
+    g_create_error = h->err;
+    if (h->comm) ncclCommDestroy(h->comm);
+    free_all(h);
+    if (h->own_stream) cudaStreamDestroy(h->own_stream);
+    delete h;
+    return r;
+  }
+  *out = h;
+  return OSBLI_OK;
+}
+
+int osbli_local_box(const osbli_ctx *h, int *z0, int *nz_local) {
+  if (!h || !z0 || !nz_local) return OSBLI_E_INVAL;
+  *z0 = h->z0;
+  *nz_local = h->nz;
+  return OSBLI_OK;
+}
+
+int osbli_set_stream(osbli_ctx *h, void *cuda_stream) {
+  int u = check_usable(h);
+  if (u) return u;
+  // order the switch: work queued on the old stream completes first
+  CK(h, cudaStreamSynchronize(h->stream));
+  h->stream = cuda_stream ? (cudaStream_t)cuda_stream : h->own_stream;
+  return OSBLI_OK;
+}
+
+int osbli_set_state(osbli_ctx *h, const double *q, int on_device) {
+  int u = check_usable(h);
+  if (u) return u;
+  if (!q) return fail(h, OSBLI_E_INVAL, "null state pointer");
+  const size_t n = (size_t)5 * h->nz * h->nx * h->ny;
+  // stage in ABI layout through the z-pass scratch (Rz), then transpose
+  CK(h, cudaMemcpyAsync(h->b.rz, q, n * sizeof(double),
+                        on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, h->stream));
+  CK(h, osbli::launch_abi_to_internal(h->base, h->b.rz, h->b.q[h->cur], h->stream, &h->launches));
+  CK(h, cudaMemsetAsync(h->b.flag, 0, sizeof(unsigned int), h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  h->step_count = 0;
+  return OSBLI_OK;
+}
+
+int osbli_get_state(osbli_ctx *h, double *q, int on_device) {
+  if (!h || !q) return OSBLI_E_INVAL;
+  const size_t n = (size_t)5 * h->nz * h->nx * h->ny;
+  CK(h, osbli::launch_internal_to_abi(h->base, h->b.q[h->cur], h->b.rz, 5, 1, h->stream, &h->launches));
+  CK(h, cudaMemcpyAsync(q, h->b.rz, n * sizeof(double),
+                        on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  return OSBLI_OK;
+}
+
+int osbli_step(osbli_ctx *h, int n) {
+  int u = check_usable(h);
+  if (u) return u;
+  if (n < 0) return fail(h, OSBLI_E_INVAL, "n must be >= 0");
+  static const double RK_A[3] = {0.0, -5.0 / 9.0, -153.0 / 128.0};
+  static const double RK_B[3] = {1.0 / 3.0, 15.0 / 16.0, 8.0 / 15.0};
+  const int nst = (h->scheme == OSBLI_RK3) ? 3 : 1;
+  for (int it = 0; it < n; ++it) {
+    for (int s = 0; s < nst; ++s) {
+      KParams p = h->base;
+      if (h->scheme == OSBLI_RK3) {
+        p.A = RK_A[s];
+        p.B = RK_B[s];
+        p.read_w = (s > 0);
+        p.write_w = (s < 2);
+      } else {
+        p.A = 0.0;
+        p.B = 1.0;
+        p.read_w = 0;
+        p.write_w = 0;
+      }
+      double *qin = h->b.q[h->cur], *qout = h->b.q[h->cur ^ 1];
+      int r = exchange_ghosts(h, qin);
+      if (r) return r;
+      CK(h, osbli::launch_stage(p, qin, qout, h->b.w, h->b.rz, h->b.gz, nullptr, h->b.flag,
+                                h->stream, &h->launches));
+      h->cur ^= 1;
+    }
+    ++h->step_count;
+  }
+  return OSBLI_OK;
+}
+
+int osbli_residual(osbli_ctx *h, double *R, int on_device) {
+  int u = check_usable(h);
+  if (u) return u;
+  if (!R) return fail(h, OSBLI_E_INVAL, "null output pointer");
+  const size_t n = (size_t)5 * h->nz * h->nx * h->ny;
+  double *qin = h->b.q[h->cur];
+  int r = exchange_ghosts(h, qin);
+  if (r) return r;
+  // R lands in W ([nz][5] plane-major), then is transposed into Rz (ABI layout)
+  CK(h, osbli::launch_stage(h->base, qin, nullptr, h->b.w, h->b.rz, h->b.gz, h->b.w, h->b.flag,
+                            h->stream, &h->launches));
+  CK(h, osbli::launch_internal_to_abi(h->base, h->b.w, h->b.rz, 5, 0, h->stream, &h->launches));
+  CK(h, cudaMemcpyAsync(R, h->b.rz, n * sizeof(double),
+                        on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  return OSBLI_OK;
+}
+
+int osbli_diagnostics(osbli_ctx *h, osbli_diag *out) {
+  int u = check_usable(h);
+  if (u) return u;
+  if (!out) return fail(h, OSBLI_E_INVAL, "null output pointer");
+  int r = check_flag(h);
+  if (r) return r;
+  double *qin = h->b.q[h->cur];
+  r = exchange_ghosts(h, qin);
+  if (r) return r;
+  CK(h, osbli::launch_diagnostics(h->base, qin, h->scratch, h->b.diag_part, h->stream,
+                                  &h->launches));
+  std::vector<double> all;
+  std::vector<int> counts;
+  if (h->nranks > 1) {
+    const int base = h->nz_global / h->nranks, extra = h->nz_global % h->nranks;
+    CK(h, cudaMemsetAsync(h->nccl_part, 0, (size_t)3 * h->nranks * h->max_nz * sizeof(double),
+                          h->stream));
+    // gather padded per-plane partials; every rank then sums in global plane order
+    NK(h, ncclAllGather(h->b.diag_part, h->nccl_part, (size_t)3 * h->max_nz, ncclDouble, h->comm,
+                        h->stream));
+    all.resize((size_t)3 * h->nranks * h->max_nz);
+    CK(h, cudaMemcpyAsync(all.data(), h->nccl_part, all.size() * sizeof(double),
+                          cudaMemcpyDeviceToHost, h->stream));
+    for (int rr = 0; rr < h->nranks; ++rr) counts.push_back(base + (rr < extra ? 1 : 0));
+  } else {
+    all.resize((size_t)3 * h->nz);
+    CK(h, cudaMemcpyAsync(all.data(), h->b.diag_part, all.size() * sizeof(double),
+                          cudaMemcpyDeviceToHost, h->stream));
+    counts.push_back(h->nz);
+  }
+  CK(h, cudaStreamSynchronize(h->stream));
+  // Neumaier sums over planes in global z order
+  double s[3] = {0, 0, 0}, c[3] = {0, 0, 0};
+  const int stride = (h->nranks > 1) ? h->max_nz : h->nz;
+  for (int rr = 0; rr < (int)counts.size(); ++rr)
+    for (int z = 0; z < counts[rr]; ++z)
+      for (int k = 0; k < 3; ++k) {
+        const double x = all[(size_t)3 * ((size_t)rr * stride + z) + k];
+        const double t = s[k] + x;
+        if (std::fabs(s[k]) >= std::fabs(x)) c[k] += (s[k] - t) + x;
+        else c[k] += (x - t) + s[k];
+        s[k] = t;
+      }
+  const double N = (double)h->nx * h->ny * h->nz_global;
+  out->t = h->step_count * h->dt;
+  out->step = h->step_count;
+  out->kinetic_energy = (s[0] + c[0]) / N;
+  out->enstrophy = (s[1] + c[1]) / N;
+  out->dissipation = (s[2] + c[2]) / N;
+  return OSBLI_OK;
+}
+
+int osbli_sync(osbli_ctx *h) {
+  int u = check_usable(h);
+  if (u) return u;
+  return check_flag(h);
+}
+
+long long osbli_kernel_launches(const osbli_ctx *h) { return h ? h->launches : -1; }
+
+const char *osbli_last_error(const osbli_ctx *h) {
+  return h ? h->err.c_str() : g_create_error.c_str();
+}
+
+void osbli_destroy(osbli_ctx *h) {
+  if (!h) return;
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  if (h->comm) ncclCommDestroy(h->comm);
+  free_all(h);
+  if (h->own_stream) cudaStreamDestroy(h->own_stream);
+  delete h;
+}
+
+}  // extern "C"

@@ -1,0 +1,640 @@
+// =============================================================================
+// sm_100a fp64 kernels of the OpenSBLI hot path (B200-native).
+//
+// One RK stage = two kernels:
+//   zpass  : every term of the residual that differentiates along z
+//            (D_z, D_zz; P:271-274 skew terms, P:274 Laplacians), written as a
+//            partial residual Rz[5] plus the velocity gradients g_i2 = D_z u_i.
+//            A CTA stages 32 x-columns x (TZ+2m) z-planes of the 13 z-stencil
+//            operands in shared memory (computed once per staged point) and
+//            each thread produces RZ = 4 consecutive z outputs from a register
+//            window (reuse (RZ+2m)/RZ instead of 2m loads per output).
+//   xypass : all x/y terms on a 32x8 plane tile with an m-wide halo in
+//            shared memory, the mixed derivatives (commuted so that no z
+//            stencil is needed: D_x D_z u_z = D_x g_22, D_z D_x u_x = D_x g_02,
+//            ...; D-7), the viscous dissipation and heat flux, then
+//            the fused low-storage RK stage update W <- A W + dt R,
+//            Q' <- Q + B W and a non-finite check.
+// All arithmetic is IEEE fp64; tensor cores are not used (a stencil is not a
+// dense contraction).  Periodic wrap in x and y is done in-kernel; in
+// z either in-kernel (one GPU) or through ghost planes (slab decomposition).
+// =============================================================================
+#include <cstdint>
+
+#include "kernels.h"
+
+namespace osbli {
+namespace {
+
+__device__ __forceinline__ int wrapi(int i, int n) {
+  int r = i % n;
+  return r < 0 ? r + n : r;
+}
+
+__device__ __forceinline__ size_t qplane(const KParams &p, int z) {
+  return (size_t)(z + p.G) * 5 * (size_t)p.nx * p.ny;
+}
+
+// z index of the plane read for logical plane z (wrap on one GPU, ghosts otherwise)
+__device__ __forceinline__ int zread(const KParams &p, int z) {
+  if (p.zwrap) return wrapi(z, p.nz);
+  return max(-p.G, min(z, p.nz - 1 + p.G));
+}
+
+// ------------------------------------------------------------------ z-pass
+constexpr int ZP_TX = 32;
+constexpr int ZP_TZ = 32;
+constexpr int ZP_RZ = 4;
+constexpr int ZP_THREADS = 32 * (ZP_TZ / ZP_RZ);  // 256
+constexpr int ZP_NF = 13;
+// staged operand slots
+enum { ZS_RHO = 0, ZS_M0, ZS_M1, ZS_M2, ZS_E, ZS_U0, ZS_U1, ZS_U2, ZS_T, ZS_F0, ZS_F1, ZS_F2, ZS_G };
+
+template <int M>
+constexpr int zp_smem_bytes() {
+  return ZP_NF * (ZP_TZ + 2 * M) * 32 * (int)sizeof(double);
+}
+
+template <int M>
+__device__ __forceinline__ void zwindow(const double *S, int f, int pbase, int lane,
+                                        double (&v)[ZP_RZ + 2 * M]) {
+  constexpr int NP = ZP_TZ + 2 * M;
+#pragma unroll
+  for (int t = 0; t < ZP_RZ + 2 * M; ++t) v[t] = S[(f * NP + pbase + t) * 32 + lane];
+}
+
+template <int M>
+__device__ __forceinline__ double d1w(const KParams &p, const double (&v)[ZP_RZ + 2 * M], int j) {
+  double s = 0.0;
+#pragma unroll
+  for (int k = 1; k <= M; ++k) s = fma(p.a[k - 1], v[j + M + k] - v[j + M - k], s);
+  return s;
+}
+
+template <int M>
+__device__ __forceinline__ double d2w(const KParams &p, const double (&v)[ZP_RZ + 2 * M], int j) {
+  const double c = v[j + M];
+  double s = 0.0;
+#pragma unroll
+  for (int k = 1; k <= M; ++k) s = fma(p.b[k], (v[j + M + k] - c) + (v[j + M - k] - c), s);
+  return s;
+}
+
+template <int M>
+__global__ void __launch_bounds__(ZP_THREADS, 1)
+    zpass_kernel(const KParams p, const double *__restrict__ q, double *__restrict__ rz,
+                 double *__restrict__ gz, int z_begin, int z_end) {
+  extern __shared__ double S[];
+  constexpr int NP = ZP_TZ + 2 * M;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int x0 = blockIdx.x * ZP_TX, y = blockIdx.y;
+  const int z0 = z_begin + blockIdx.z * ZP_TZ;
+  const size_t FS = (size_t)p.nx * p.ny;
+
+  // ---- stage the z-stencil operands of NP planes x 32 columns (formulas)
+  for (int idx = threadIdx.x; idx < NP * 32; idx += ZP_THREADS) {
+    const int pl = idx >> 5, c = idx & 31;
+    int x = x0 + c;
+    if (x >= p.nx) x = wrapi(x, p.nx);
+    const int z = zread(p, z0 - M + pl);
+    const double *qp = q + qplane(p, z) + (size_t)y * p.nx + x;
+    const double rho = qp[0], m0 = qp[FS], m1 = qp[2 * FS], m2 = qp[3 * FS], e = qp[4 * FS];
+    const double r = 1.0 / rho;
+    const double u0 = m0 * r, u1 = m1 * r, u2 = m2 * r;
+    const double pr = p.gm1 * (e - 0.5 * (m0 * u0 + m1 * u1 + m2 * u2));
+    const double T = p.gM2 * pr * r;
+    double *s = S + pl * 32 + c;
+    s[ZS_RHO * NP * 32] = rho;
+    s[ZS_M0 * NP * 32] = m0;
+    s[ZS_M1 * NP * 32] = m1;
+    s[ZS_M2 * NP * 32] = m2;
+    s[ZS_E * NP * 32] = e;
+    s[ZS_U0 * NP * 32] = u0;
+    s[ZS_U1 * NP * 32] = u1;
+    s[ZS_U2 * NP * 32] = u2;
+    s[ZS_T * NP * 32] = T;
+    // momentum flux F_i2 = 1/2 m_i u_2 + delta_i2 p  (skew half + pressure)
+    s[ZS_F0 * NP * 32] = 0.5 * m0 * u2;
+    s[ZS_F1 * NP * 32] = 0.5 * m1 * u2;
+    s[ZS_F2 * NP * 32] = 0.5 * m2 * u2 + pr;
+    // energy flux G_2 = (1/2 e + p) u_2  (skew half + pressure work)
+    s[ZS_G * NP * 32] = (0.5 * e + pr) * u2;
+  }
+  __syncthreads();
+
+  const int pbase = warp * ZP_RZ;
+  double v[ZP_RZ + 2 * M];
+  double g[3][ZP_RZ], R[5][ZP_RZ], u2c[ZP_RZ];
+
+  // velocity: g_i2 = D_z u_i, viscous z-Laplacian parts of V_i and u_i V_i
+  zwindow<M>(S, ZS_U2, pbase, lane, v);
+  double d2u2[ZP_RZ];
+#pragma unroll
+  for (int j = 0; j < ZP_RZ; ++j) {
+    g[2][j] = d1w<M>(p, v, j);
+    d2u2[j] = d2w<M>(p, v, j);
+    u2c[j] = v[j + M];
+    const double V2 = p.nu * (d2u2[j] + (1.0 / 3.0) * d2u2[j]);
+    R[3][j] = V2;
+    R[4][j] = u2c[j] * V2;
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    zwindow<M>(S, ZS_U0 + i, pbase, lane, v);
+#pragma unroll
+    for (int j = 0; j < ZP_RZ; ++j) {
+      g[i][j] = d1w<M>(p, v, j);
+      const double Vi = p.nu * d2w<M>(p, v, j);
+      R[1 + i][j] = Vi;
+      R[4][j] = fma(v[j + M], Vi, R[4][j]);
+    }
+  }
+  // heat flux: kappa D_zz T
+  zwindow<M>(S, ZS_T, pbase, lane, v);
+#pragma unroll
+  for (int j = 0; j < ZP_RZ; ++j) R[4][j] = fma(p.kappa, d2w<M>(p, v, j), R[4][j]);
+  // skew advective + dilatation halves: -1/2 (u_2 D_z s + s g_22) for s = rho, m_i, e
+#pragma unroll
+  for (int f = 0; f < 5; ++f) {
+    zwindow<M>(S, ZS_RHO + f, pbase, lane, v);
+#pragma unroll
+    for (int j = 0; j < ZP_RZ; ++j) {
+      const double ds = d1w<M>(p, v, j);
+      const double t = fma(u2c[j], ds, v[j + M] * g[2][j]);
+      if (f == 0) R[0][j] = -0.5 * t;
+      else R[f][j] = fma(-0.5, t, R[f][j]);
+      if (f == 3) R[0][j] = fma(-0.5, ds, R[0][j]);  // mass flux D_z(rho u_2) = D_z m_2
+    }
+  }
+  // conservative flux halves: -D_z F_i2, -D_z G_2
+#pragma unroll
+  for (int f = 0; f < 4; ++f) {
+    zwindow<M>(S, ZS_F0 + f, pbase, lane, v);
+#pragma unroll
+    for (int j = 0; j < ZP_RZ; ++j) R[1 + f][j] -= d1w<M>(p, v, j);
+  }
+
+  const int x = x0 + lane;
+  if (x < p.nx) {
+#pragma unroll
+    for (int j = 0; j < ZP_RZ; ++j) {
+      const int z = z0 + pbase + j;
+      if (z < z_end) {
+        const size_t o = (size_t)z * 5 * FS + (size_t)y * p.nx + x;
+#pragma unroll
+        for (int f = 0; f < 5; ++f) rz[o + f * FS] = R[f][j];
+        const size_t og = (size_t)z * 3 * FS + (size_t)y * p.nx + x;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) gz[og + i * FS] = g[i][j];
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ xy-pass
+constexpr int XY_TX = 32;
+constexpr int XY_TY = 8;
+constexpr int XY_THREADS = XY_TX * XY_TY;  // 256
+constexpr int XY_NF = 13;
+enum { XS_RHO = 0, XS_M0, XS_M1, XS_M2, XS_E, XS_U0, XS_U1, XS_U2, XS_P, XS_T, XS_G02, XS_G12, XS_G22 };
+
+template <int M>
+constexpr int xy_smem_bytes() {
+  return (XY_NF * (XY_TX + 2 * M) * (XY_TY + 2 * M) + 2 * XY_TX * (XY_TY + 2 * M)) *
+         (int)sizeof(double);
+}
+
+template <int M, int STRIDE>
+__device__ __forceinline__ double d1s(const KParams &p, const double *f, int c) {
+  double s = 0.0;
+#pragma unroll
+  for (int k = 1; k <= M; ++k) s = fma(p.a[k - 1], f[c + k * STRIDE] - f[c - k * STRIDE], s);
+  return s;
+}
+
+template <int M, int STRIDE>
+__device__ __forceinline__ double d2s(const KParams &p, const double *f, int c) {
+  const double f0 = f[c];
+  double s = 0.0;
+#pragma unroll
+  for (int k = 1; k <= M; ++k)
+    s = fma(p.b[k], (f[c + k * STRIDE] - f0) + (f[c - k * STRIDE] - f0), s);
+  return s;
+}
+
+// first derivative of the product (alpha * f * h + beta * e), taps from smem
+template <int M, int STRIDE>
+__device__ __forceinline__ double d1prod(const KParams &p, const double *f, const double *h,
+                                         const double *add, double alpha, int c) {
+  double s = 0.0;
+#pragma unroll
+  for (int k = 1; k <= M; ++k) {
+    const int cp = c + k * STRIDE, cm = c - k * STRIDE;
+    double vp = alpha * f[cp] * h[cp];
+    double vm = alpha * f[cm] * h[cm];
+    if (add) {
+      vp += add[cp];
+      vm += add[cm];
+    }
+    s = fma(p.a[k - 1], vp - vm, s);
+  }
+  return s;
+}
+
+template <int M>
+__global__ void __launch_bounds__(XY_THREADS, 2)
+    xypass_kernel(const KParams p, const double *__restrict__ q, double *__restrict__ qout,
+                  double *__restrict__ w, const double *__restrict__ rz,
+                  const double *__restrict__ gz, double *__restrict__ rout,
+                  unsigned int *__restrict__ flag, int z_begin) {
+  constexpr int HX = XY_TX + 2 * M, HY = XY_TY + 2 * M, HN = HX * HY;
+  extern __shared__ double S[];
+  double *E = S + XY_NF * HN;  // [2][HY][32]: g00, g10 on the y-extended tile
+  const int z = z_begin + blockIdx.z;
+  const int x0 = blockIdx.x * XY_TX, y0 = blockIdx.y * XY_TY;
+  const size_t FS = (size_t)p.nx * p.ny;
+  const double *qp = q + qplane(p, z);
+  const double *gp = gz + (size_t)z * 3 * FS;
+
+  // ---- stage tile + halo (formulas; EOS P:259-266)
+  for (int idx = threadIdx.x; idx < HN; idx += XY_THREADS) {
+    const int hx = idx % HX, hy = idx / HX;
+    const int x = wrapi(x0 - M + hx, p.nx), y = wrapi(y0 - M + hy, p.ny);
+    const size_t off = (size_t)y * p.nx + x;
+    const double rho = qp[off], m0 = qp[FS + off], m1 = qp[2 * FS + off], m2 = qp[3 * FS + off],
+                 e = qp[4 * FS + off];
+    const double r = 1.0 / rho;
+    const double u0 = m0 * r, u1 = m1 * r, u2 = m2 * r;
+    const double pr = p.gm1 * (e - 0.5 * (m0 * u0 + m1 * u1 + m2 * u2));
+    S[XS_RHO * HN + idx] = rho;
+    S[XS_M0 * HN + idx] = m0;
+    S[XS_M1 * HN + idx] = m1;
+    S[XS_M2 * HN + idx] = m2;
+    S[XS_E * HN + idx] = e;
+    S[XS_U0 * HN + idx] = u0;
+    S[XS_U1 * HN + idx] = u1;
+    S[XS_U2 * HN + idx] = u2;
+    S[XS_P * HN + idx] = pr;
+    S[XS_T * HN + idx] = p.gM2 * pr * r;
+    S[XS_G02 * HN + idx] = gp[off];
+    S[XS_G12 * HN + idx] = gp[FS + off];
+    S[XS_G22 * HN + idx] = gp[2 * FS + off];
+  }
+  __syncthreads();
+  // ---- inner derivatives g00 = D_x u0, g10 = D_x u1 on the y-extended tile
+  //      (the nested derivatives D_y g00, D_y g10)
+  for (int idx = threadIdx.x; idx < XY_TX * HY; idx += XY_THREADS) {
+    const int tx = idx & 31, hy = idx >> 5;
+    const int c = hy * HX + tx + M;
+    E[idx] = d1s<M, 1>(p, S + XS_U0 * HN, c);
+    E[XY_TX * HY + idx] = d1s<M, 1>(p, S + XS_U1 * HN, c);
+  }
+  __syncthreads();
+
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int c = (ty + M) * HX + tx + M;
+  const int ce = (ty + M) * XY_TX + tx;
+  const double *Srho = S + XS_RHO * HN, *Sm0 = S + XS_M0 * HN, *Sm1 = S + XS_M1 * HN,
+               *Sm2 = S + XS_M2 * HN, *Se = S + XS_E * HN, *Su0 = S + XS_U0 * HN,
+               *Su1 = S + XS_U1 * HN, *Su2 = S + XS_U2 * HN, *Sp = S + XS_P * HN,
+               *ST = S + XS_T * HN;
+  const double rho = Srho[c], m0 = Sm0[c], m1 = Sm1[c], m2 = Sm2[c], e = Se[c];
+  const double u0 = Su0[c], u1 = Su1[c], u2 = Su2[c];
+  const double g02 = S[XS_G02 * HN + c], g12 = S[XS_G12 * HN + c], g22 = S[XS_G22 * HN + c];
+
+  // ---- velocity gradients and viscous terms
+  const double g00 = d1s<M, 1>(p, Su0, c), g10 = d1s<M, 1>(p, Su1, c), g20 = d1s<M, 1>(p, Su2, c);
+  const double g01 = d1s<M, HX>(p, Su0, c), g11 = d1s<M, HX>(p, Su1, c), g21 = d1s<M, HX>(p, Su2, c);
+  const double d00u0 = d2s<M, 1>(p, Su0, c), d11u0 = d2s<M, HX>(p, Su0, c);
+  const double d00u1 = d2s<M, 1>(p, Su1, c), d11u1 = d2s<M, HX>(p, Su1, c);
+  const double d00u2 = d2s<M, 1>(p, Su2, c), d11u2 = d2s<M, HX>(p, Su2, c);
+  // mixed (commuted, D-7): D_x g11 -> D_y g10 ; D_y g00 ; D_x g22 ; D_y g22 ;
+  // D_z g00 -> D_x g02 ; D_z g11 -> D_y g12
+  const double dy_g10 = d1s<M, XY_TX>(p, E + XY_TX * HY, ce);
+  const double dy_g00 = d1s<M, XY_TX>(p, E, ce);
+  const double dx_g22 = d1s<M, 1>(p, S + XS_G22 * HN, c);
+  const double dy_g22 = d1s<M, HX>(p, S + XS_G22 * HN, c);
+  const double dx_g02 = d1s<M, 1>(p, S + XS_G02 * HN, c);
+  const double dy_g12 = d1s<M, HX>(p, S + XS_G12 * HN, c);
+  const double third = 1.0 / 3.0;
+  // V_i (x,y parts) = nu [ D_xx u_i + D_yy u_i + 1/3 ( D_ii u_i + sum_{j != i} D_i D_j u_j ) ]
+  const double V0 = p.nu * (d00u0 + d11u0 + third * (d00u0 + dy_g10 + dx_g22));
+  const double V1 = p.nu * (d00u1 + d11u1 + third * (d11u1 + dy_g00 + dy_g22));
+  const double V2 = p.nu * (d00u2 + d11u2 + third * (dx_g02 + dy_g12));
+
+  // ---- skew-symmetric convection, x and y parts
+  const double th_xy = g00 + g11;
+  double R[5];
+  {
+    const double drx = d1s<M, 1>(p, Srho, c), dry = d1s<M, HX>(p, Srho, c);
+    const double dm0x = d1s<M, 1>(p, Sm0, c), dm1y = d1s<M, HX>(p, Sm1, c);
+    R[0] = -0.5 * (dm0x + dm1y + u0 * drx + u1 * dry + rho * th_xy);
+  }
+  const double *Sm[3] = {Sm0, Sm1, Sm2};
+  const double mc[3] = {m0, m1, m2};
+  const double Vv[3] = {V0, V1, V2};
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const double dmx = d1s<M, 1>(p, Sm[i], c), dmy = d1s<M, HX>(p, Sm[i], c);
+    // F_i0 = 1/2 m_i u_0 + delta_i0 p ; F_i1 = 1/2 m_i u_1 + delta_i1 p
+    const double dFx = d1prod<M, 1>(p, Sm[i], Su0, i == 0 ? Sp : nullptr, 0.5, c);
+    const double dFy = d1prod<M, HX>(p, Sm[i], Su1, i == 1 ? Sp : nullptr, 0.5, c);
+    R[1 + i] = -(dFx + dFy + 0.5 * (u0 * dmx + u1 * dmy + mc[i] * th_xy)) + Vv[i];
+  }
+  {
+    const double dex = d1s<M, 1>(p, Se, c), dey = d1s<M, HX>(p, Se, c);
+    // G_j = (1/2 e + p) u_j
+    double dGx = 0.0, dGy = 0.0;
+#pragma unroll
+    for (int k = 1; k <= M; ++k) {
+      const int cp = c + k, cm = c - k;
+      dGx = fma(p.a[k - 1], (0.5 * Se[cp] + Sp[cp]) * Su0[cp] - (0.5 * Se[cm] + Sp[cm]) * Su0[cm], dGx);
+      const int dp = c + k * HX, dm = c - k * HX;
+      dGy = fma(p.a[k - 1], (0.5 * Se[dp] + Sp[dp]) * Su1[dp] - (0.5 * Se[dm] + Sp[dm]) * Su1[dm], dGy);
+    }
+    const double heat = p.kappa * (d2s<M, 1>(p, ST, c) + d2s<M, HX>(p, ST, c));
+    const double th = th_xy + g22;
+    const double s01 = g01 + g10, s02 = g02 + g20, s12 = g12 + g21;
+    // viscous dissipation tau_ij g_ij (eq. 8) = nu [2 sum g_ii^2 + sum_{i<j} (g_ij+g_ji)^2 - 2/3 th^2]
+    const double Phi = p.nu * (2.0 * (g00 * g00 + g11 * g11 + g22 * g22) + s01 * s01 + s02 * s02 +
+                               s12 * s12 - (2.0 / 3.0) * th * th);
+    R[4] = -(dGx + dGy + 0.5 * (u0 * dex + u1 * dey + e * th_xy)) + heat + Phi +
+           (u0 * V0 + u1 * V1 + u2 * V2);
+  }
+
+  // ---- epilogue: add the z-pass partial residual, RK stage update
+  const int x = x0 + tx, y = y0 + ty;
+  if (x >= p.nx || y >= p.ny) return;
+  const size_t o = (size_t)z * 5 * FS + (size_t)y * p.nx + x;
+  const double qc[5] = {rho, m0, m1, m2, e};
+  double *qo = qout ? qout + qplane(p, z) + (size_t)y * p.nx + x : nullptr;
+  bool bad = false;
+#pragma unroll
+  for (int f = 0; f < 5; ++f) {
+    const double Rf = R[f] + rz[o + f * FS];
+    if (rout) {
+      rout[o + f * FS] = Rf;
+      continue;
+    }
+    double wn = p.dt * Rf;
+    if (p.read_w) wn = fma(p.A, w[o + f * FS], wn);
+    if (p.write_w) w[o + f * FS] = wn;
+    const double qn = fma(p.B, wn, qc[f]);
+    qo[f * FS] = qn;
+    bad |= !isfinite(qn);
+  }
+  if (bad) atomicOr(flag, 1u);
+}
+
+// ------------------------------------------------------------------ diagnostics
+__global__ void velocity_kernel(const KParams p, const double *__restrict__ q,
+                                double *__restrict__ u, int zlo, int zhi) {
+  const size_t FS = (size_t)p.nx * p.ny;
+  const size_t n = (size_t)(zhi - zlo) * FS;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < n;
+       t += (size_t)gridDim.x * blockDim.x) {
+    const int z = zlo + (int)(t / FS);
+    const size_t off = t % FS;
+    const double *qp = q + qplane(p, z) + off;
+    const double r = 1.0 / qp[0];
+    double *up = u + (size_t)(z + p.G) * 3 * FS + off;
+    up[0] = qp[FS] * r;
+    up[FS] = qp[2 * FS] * r;
+    up[2 * FS] = qp[3 * FS] * r;
+  }
+}
+
+template <int M>
+__global__ void __launch_bounds__(256) diag_kernel(const KParams p, const double *__restrict__ q,
+                                                   const double *__restrict__ u,
+                                                   double *__restrict__ part) {
+  const int z = blockIdx.x;
+  const size_t FS = (size_t)p.nx * p.ny;
+  double sk = 0.0, se = 0.0, sd = 0.0;
+  for (int t = threadIdx.x; t < (int)FS; t += blockDim.x) {
+    const int x = t % p.nx, y = t / p.nx;
+    const double *qp = q + qplane(p, z) + t;
+    double g[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const double *ui = u + 3 * FS * 0 + (size_t)i * FS;
+      double sx = 0.0, sy = 0.0, sz = 0.0;
+#pragma unroll
+      for (int k = 1; k <= M; ++k) {
+        const size_t rowp = (size_t)y * p.nx, zp_ = (size_t)(zread(p, z + k) + p.G) * 3 * FS,
+                     zm_ = (size_t)(zread(p, z - k) + p.G) * 3 * FS,
+                     z0_ = (size_t)(z + p.G) * 3 * FS;
+        sx = fma(p.a[k - 1],
+                 ui[z0_ + rowp + wrapi(x + k, p.nx)] - ui[z0_ + rowp + wrapi(x - k, p.nx)], sx);
+        sy = fma(p.a[k - 1],
+                 ui[z0_ + (size_t)wrapi(y + k, p.ny) * p.nx + x] -
+                     ui[z0_ + (size_t)wrapi(y - k, p.ny) * p.nx + x],
+                 sy);
+        sz = fma(p.a[k - 1], ui[zp_ + rowp + x] - ui[zm_ + rowp + x], sz);
+      }
+      g[i][0] = sx;
+      g[i][1] = sy;
+      g[i][2] = sz;
+    }
+    const double rho = qp[0];
+    const double *uc = u + (size_t)(z + p.G) * 3 * FS + t;
+    const double u0 = uc[0], u1 = uc[FS], u2 = uc[2 * FS];
+    sk += 0.5 * rho * (u0 * u0 + u1 * u1 + u2 * u2);
+    const double w0 = g[2][1] - g[1][2], w1 = g[0][2] - g[2][0], w2 = g[1][0] - g[0][1];
+    se += 0.5 * rho * (w0 * w0 + w1 * w1 + w2 * w2);
+    const double th = g[0][0] + g[1][1] + g[2][2];
+    const double s01 = g[0][1] + g[1][0], s02 = g[0][2] + g[2][0], s12 = g[1][2] + g[2][1];
+    sd += p.nu * (2.0 * (g[0][0] * g[0][0] + g[1][1] * g[1][1] + g[2][2] * g[2][2]) +
+                  s01 * s01 + s02 * s02 + s12 * s12 - (2.0 / 3.0) * th * th);
+  }
+  // fixed-shape tree reduction -> deterministic, decomposition-independent
+  __shared__ double red[3][256];
+  red[0][threadIdx.x] = sk;
+  red[1][threadIdx.x] = se;
+  red[2][threadIdx.x] = sd;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if ((int)threadIdx.x < s) {
+      red[0][threadIdx.x] += red[0][threadIdx.x + s];
+      red[1][threadIdx.x] += red[1][threadIdx.x + s];
+      red[2][threadIdx.x] += red[2][threadIdx.x + s];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    part[3 * z + 0] = red[0][0];
+    part[3 * z + 1] = red[1][0];
+    part[3 * z + 2] = red[2][0];
+  }
+}
+
+// ------------------------------------------------------------------ layout conversion
+__global__ void abi_to_internal_kernel(const KParams p, const double *__restrict__ src,
+                                       double *__restrict__ q) {
+  const size_t FS = (size_t)p.nx * p.ny;
+  const size_t n = 5 * FS * p.nz;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < n;
+       t += (size_t)gridDim.x * blockDim.x) {
+    const size_t f = t / (FS * p.nz), rem = t % (FS * p.nz);
+    const int z = (int)(rem / FS);
+    const size_t off = rem % FS;
+    q[qplane(p, z) + f * FS + off] = src[t];
+  }
+}
+
+__global__ void internal_to_abi_kernel(const KParams p, const double *__restrict__ q,
+                                       double *__restrict__ dst, int nfields, int ghosted) {
+  const size_t FS = (size_t)p.nx * p.ny;
+  const size_t n = (size_t)nfields * FS * p.nz;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < n;
+       t += (size_t)gridDim.x * blockDim.x) {
+    const size_t f = t / (FS * p.nz), rem = t % (FS * p.nz);
+    const int z = (int)(rem / FS);
+    const size_t off = rem % FS;
+    const size_t plane = ghosted ? (size_t)(z + p.G) : (size_t)z;
+    dst[t] = q[plane * nfields * FS + f * FS + off];
+  }
+}
+
+template <int M>
+cudaError_t zpass_launch(const KParams &p, const double *q, double *rz, double *gz, int zb, int ze,
+                         cudaStream_t s) {
+  constexpr int smem = zp_smem_bytes<M>();
+  static bool init = false;
+  if (!init) {
+    cudaError_t e =
+        cudaFuncSetAttribute(zpass_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    init = true;
+  }
+  dim3 grid((p.nx + ZP_TX - 1) / ZP_TX, p.ny, (ze - zb + ZP_TZ - 1) / ZP_TZ);
+  zpass_kernel<M><<<grid, ZP_THREADS, smem, s>>>(p, q, rz, gz, zb, ze);
+  return cudaGetLastError();
+}
+
+template <int M>
+cudaError_t xypass_launch(const KParams &p, const double *q, double *qout, double *w,
+                          const double *rz, const double *gz, double *rout, unsigned int *flag,
+                          int zb, int ze, cudaStream_t s) {
+  constexpr int smem = xy_smem_bytes<M>();
+  static bool init = false;
+  if (!init) {
+    cudaError_t e =
+        cudaFuncSetAttribute(xypass_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    init = true;
+  }
+  dim3 grid((p.nx + XY_TX - 1) / XY_TX, (p.ny + XY_TY - 1) / XY_TY, ze - zb);
+  xypass_kernel<M><<<grid, XY_THREADS, smem, s>>>(p, q, qout, w, rz, gz, rout, flag, zb);
+  return cudaGetLastError();
+}
+
+template <int M>
+cudaError_t diag_launch(const KParams &p, const double *q, const double *u, double *part,
+                        cudaStream_t s) {
+  diag_kernel<M><<<p.nz, 256, 0, s>>>(p, q, u, part);
+  return cudaGetLastError();
+}
+
+int grid1d(size_t n) {
+  size_t b = (n + 255) / 256;
+  if (b > 148 * 16) b = 148 * 16;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+}  // namespace
+
+#define OSBLI_DISPATCH_M(m, CALL) \
+  switch (m) {                    \
+    case 1: return CALL<1>;       \
+    case 2: return CALL<2>;       \
+    case 3: return CALL<3>;       \
+    case 4: return CALL<4>;       \
+    case 5: return CALL<5>;       \
+    case 6: return CALL<6>;       \
+    default: return cudaErrorInvalidValue; \
+  }
+
+cudaError_t launch_zpass(const KParams &p, const double *q_in, double *rz, double *gz, int zb,
+                         int ze, cudaStream_t s, long long *launches) {
+  if (ze <= zb) return cudaSuccess;
+  ++*launches;
+#define ZCALL(MM) zpass_launch<MM>(p, q_in, rz, gz, zb, ze, s)
+  switch (p.m) {
+    case 1: return ZCALL(1);
+    case 2: return ZCALL(2);
+    case 3: return ZCALL(3);
+    case 4: return ZCALL(4);
+    case 5: return ZCALL(5);
+    case 6: return ZCALL(6);
+    default: return cudaErrorInvalidValue;
+  }
+#undef ZCALL
+}
+
+cudaError_t launch_xypass(const KParams &p, const double *q_in, double *q_out, double *w,
+                          const double *rz, const double *gz, double *r_out, unsigned int *flag,
+                          int zb, int ze, cudaStream_t s, long long *launches) {
+  if (ze <= zb) return cudaSuccess;
+  ++*launches;
+#define XCALL(MM) xypass_launch<MM>(p, q_in, q_out, w, rz, gz, r_out, flag, zb, ze, s)
+  switch (p.m) {
+    case 1: return XCALL(1);
+    case 2: return XCALL(2);
+    case 3: return XCALL(3);
+    case 4: return XCALL(4);
+    case 5: return XCALL(5);
+    case 6: return XCALL(6);
+    default: return cudaErrorInvalidValue;
+  }
+#undef XCALL
+}
+
+cudaError_t launch_stage(const KParams &p, const double *q_in, double *q_out, double *w,
+                         double *rz, double *gz, double *r_out, unsigned int *flag,
+                         cudaStream_t s, long long *launches) {
+  cudaError_t e = launch_zpass(p, q_in, rz, gz, 0, p.nz, s, launches);
+  if (e != cudaSuccess) return e;
+  return launch_xypass(p, q_in, q_out, w, rz, gz, r_out, flag, 0, p.nz, s, launches);
+}
+
+cudaError_t launch_diagnostics(const KParams &p, const double *q_in, double *scratch,
+                               double *part, cudaStream_t s, long long *launches) {
+  // velocity on the interior planes (+ ghost planes when they are in use)
+  const int zlo = p.zwrap ? 0 : -p.G, zhi = p.zwrap ? p.nz : p.nz + p.G;
+  const size_t n = (size_t)(zhi - zlo) * p.nx * p.ny;
+  velocity_kernel<<<grid1d(n), 256, 0, s>>>(p, q_in, scratch, zlo, zhi);
+  ++*launches;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  ++*launches;
+#define DCALL(MM) diag_launch<MM>(p, q_in, scratch, part, s)
+  switch (p.m) {
+    case 1: return DCALL(1);
+    case 2: return DCALL(2);
+    case 3: return DCALL(3);
+    case 4: return DCALL(4);
+    case 5: return DCALL(5);
+    case 6: return DCALL(6);
+    default: return cudaErrorInvalidValue;
+  }
+#undef DCALL
+}
+
+cudaError_t launch_abi_to_internal(const KParams &p, const double *src, double *q, cudaStream_t s,
+                                   long long *launches) {
+  ++*launches;
+  abi_to_internal_kernel<<<grid1d(5 * (size_t)p.nx * p.ny * p.nz), 256, 0, s>>>(p, src, q);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_internal_to_abi(const KParams &p, const double *q, double *dst, int nfields,
+                                   int ghosted, cudaStream_t s, long long *launches) {
+  ++*launches;
+  internal_to_abi_kernel<<<grid1d((size_t)nfields * p.nx * p.ny * p.nz), 256, 0, s>>>(
+      p, q, dst, nfields, ghosted);
+  return cudaGetLastError();
+}
+
+}  // namespace osbli

@@ -1,0 +1,63 @@
+// Internal interface between the C-ABI runtime (api.cpp) and the sm_100a
+// kernels (kernels.cu).  Not part of the public ABI.
+#pragma once
+#include <cuda_runtime.h>
+
+namespace osbli {
+
+constexpr int kMaxHalf = 6;  // m = order/2 <= 6 (orders 2..12)
+
+// Everything a kernel needs, passed by value (lives in the constant bank).
+struct KParams {
+  int nx, ny, nz;  // local grid (nz = slab planes on this rank)
+  int G;           // ghost planes allocated on each z side of Q buffers
+  int zwrap;       // 1: single periodic domain in z (wrap modulo nz); 0: read ghost planes
+  int m;           // stencil half width
+  double a[kMaxHalf];      // first-derivative weights a_k / dx       (k = 1..m)
+  double b[kMaxHalf + 1];  // second-derivative weights b_k / dx^2    (k = 0..m)
+  double nu, kappa;        // 1/Re and 1/((gamma-1) M^2 Pr Re)  (mu = 1)
+  double gm1;              // gamma - 1
+  double gM2;              // gamma M^2
+  // stage update: W <- A W + dt R ; Q' <- Q + B W
+  double A, B, dt;
+  int read_w, write_w;     // A != 0 ; W needed by a later stage
+};
+
+// Device buffers of one handle.  Q buffers: [nz + 2G][5][ny][nx] (plane-major,
+// ghost planes at both z ends); W, Rz: [nz][5][ny][nx]; Gz: [nz][3][ny][nx].
+struct Bufs {
+  double *q[2];
+  double *w;
+  double *rz;
+  double *gz;
+  unsigned int *flag;  // non-finite flag (device)
+  double *diag_part;   // [nz][3] per-plane partial sums (device)
+};
+
+// Launch one stage: zpass(Q_in) -> Rz, Gz ; xypass -> W, Q_out (or R_out if non-null).
+// R_out (optional) is [nz][5][ny][nx].
+cudaError_t launch_stage(const KParams &p, const double *q_in, double *q_out, double *w,
+                         double *rz, double *gz, double *r_out, unsigned int *flag,
+                         cudaStream_t s, long long *launches);
+
+// z-pass restricted to planes [z_begin, z_end) (for boundary-first overlap).
+cudaError_t launch_zpass(const KParams &p, const double *q_in, double *rz, double *gz,
+                         int z_begin, int z_end, cudaStream_t s, long long *launches);
+// xy-pass restricted to planes [z_begin, z_end).
+cudaError_t launch_xypass(const KParams &p, const double *q_in, double *q_out, double *w,
+                          const double *rz, const double *gz, double *r_out, unsigned int *flag,
+                          int z_begin, int z_end, cudaStream_t s, long long *launches);
+
+// Per-plane diagnostics partial sums [nz][3] (E_k, enstrophy, dissipation sums).
+// scratch: >= 3*nx*ny*nz doubles (velocity).
+cudaError_t launch_diagnostics(const KParams &p, const double *q_in, double *scratch,
+                               double *part, cudaStream_t s, long long *launches);
+
+// Layout conversion between the ABI [5][nz][ny][nx] and the internal plane-major
+// Q buffer (interior planes only).
+cudaError_t launch_abi_to_internal(const KParams &p, const double *src, double *q, cudaStream_t s,
+                                   long long *launches);
+cudaError_t launch_internal_to_abi(const KParams &p, const double *q, double *dst, int nfields,
+                                   int ghosted, cudaStream_t s, long long *launches);
+
+}  // namespace osbli

@@ -1,0 +1,200 @@
+"""ctypes binding of include/osbli.h (argument marshalling only)."""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_ROOT = os.path.dirname(_HERE)
+_LIB_PATH = os.path.join(_HERE, "libosbli.so")
+_lib = None
+
+OSBLI_EULER = 0
+OSBLI_RK3 = 1
+_STATUS = {0: "OK", -1: "E_INVAL", -2: "E_UNSUPPORTED", -3: "E_NOMEM", -4: "E_CUDA",
+           -5: "E_COMM", -6: "E_NONFINITE", -7: "E_STATE"}
+
+
+class OsbliError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"osbli {_STATUS.get(code, code)}: {msg}")
+        self.code = code
+        self.status = _STATUS.get(code, str(code))
+
+
+def lib_path() -> str:
+    return _LIB_PATH
+
+
+def build() -> str:
+    """Compile libosbli.so for sm_100a in-tree (nvcc; no GPU needed)."""
+    subprocess.check_call(["make", "-s", "-C", _ROOT, "paper_1609_01277_b200/libosbli.so"])
+    return _LIB_PATH
+
+
+class _Diag(ctypes.Structure):
+    _fields_ = [("t", ctypes.c_double), ("step", ctypes.c_longlong),
+                ("kinetic_energy", ctypes.c_double), ("enstrophy", ctypes.c_double),
+                ("dissipation", ctypes.c_double)]
+
+
+def load():
+    """Load libosbli.so; raises if it has not been built (no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIB_PATH):
+        raise ImportError(f"{_LIB_PATH} is missing: run `make` (or __graft_entry__.build())")
+    L = ctypes.CDLL(_LIB_PATH)
+    c_int, c_double, vp = ctypes.c_int, ctypes.c_double, ctypes.c_void_p
+    H = ctypes.c_void_p
+    L.osbli_create.argtypes = [c_int, c_int, c_int, c_int, c_double, c_double, c_double, c_double,
+                               c_double, c_double, c_int, ctypes.POINTER(H)]
+    L.osbli_create_dist.argtypes = [c_int, c_int, c_int, c_int, c_double, c_double, c_double,
+                                    c_double, c_double, c_double, c_int, c_int, c_int, vp,
+                                    ctypes.POINTER(H)]
+    L.osbli_nccl_unique_id.argtypes = [vp]
+    L.osbli_local_box.argtypes = [H, ctypes.POINTER(c_int), ctypes.POINTER(c_int)]
+    L.osbli_set_stream.argtypes = [H, vp]
+    L.osbli_set_state.argtypes = [H, vp, c_int]
+    L.osbli_get_state.argtypes = [H, vp, c_int]
+    L.osbli_step.argtypes = [H, c_int]
+    L.osbli_diagnostics.argtypes = [H, ctypes.POINTER(_Diag)]
+    L.osbli_residual.argtypes = [H, vp, c_int]
+    L.osbli_sync.argtypes = [H]
+    L.osbli_kernel_launches.argtypes = [H]
+    L.osbli_kernel_launches.restype = ctypes.c_longlong
+    L.osbli_last_error.argtypes = [H]
+    L.osbli_last_error.restype = ctypes.c_char_p
+    L.osbli_version.restype = ctypes.c_char_p
+    L.osbli_destroy.argtypes = [H]
+    L.osbli_destroy.restype = None
+    _lib = L
+    return L
+
+
+def version() -> str:
+    return load().osbli_version().decode()
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    rc = load().osbli_nccl_unique_id(buf)
+    if rc != 0:
+        raise OsbliError(rc, load().osbli_last_error(None).decode())
+    return buf.raw
+
+
+def _ptr(a):
+    """(pointer, on_device) for a numpy array or a contiguous fp64 torch tensor."""
+    if isinstance(a, np.ndarray):
+        if a.dtype != np.float64 or not a.flags["C_CONTIGUOUS"]:
+            raise ValueError("state arrays must be C-contiguous float64")
+        return a.ctypes.data, 0
+    import torch  # torch only for device memory
+    if isinstance(a, torch.Tensor):
+        if a.dtype != torch.float64 or not a.is_contiguous():
+            raise ValueError("state tensors must be contiguous float64")
+        return a.data_ptr(), 1 if a.is_cuda else 0
+    raise TypeError(f"unsupported array type {type(a)}")
+
+
+@dataclass
+class Diagnostics:
+    t: float
+    step: int
+    kinetic_energy: float
+    enstrophy: float
+    dissipation: float
+
+
+class Solver:
+    """One handle of the C ABI (osbli_create / osbli_create_dist)."""
+
+    def __init__(self, nx, ny, nz, order, dx, dt, Re=1600.0, Pr=0.71, Minf=0.1, gamma=1.4,
+                 scheme=OSBLI_RK3, rank=0, nranks=1, unique_id: bytes | None = None):
+        L = load()
+        self._L = L
+        self._h = ctypes.c_void_p()
+        if nranks == 1 and unique_id is None:
+            rc = L.osbli_create(nx, ny, nz, order, dx, dt, Re, Pr, Minf, gamma, scheme,
+                                ctypes.byref(self._h))
+        else:
+            uid = ctypes.create_string_buffer(unique_id, 128) if unique_id else None
+            rc = L.osbli_create_dist(nx, ny, nz, order, dx, dt, Re, Pr, Minf, gamma, scheme,
+                                     rank, nranks, uid, ctypes.byref(self._h))
+        if rc != 0:
+            raise OsbliError(rc, L.osbli_last_error(None).decode())
+        self.nx, self.ny, self.nz_global, self.order = nx, ny, nz, order
+        z0, nzl = ctypes.c_int(), ctypes.c_int()
+        L.osbli_local_box(self._h, ctypes.byref(z0), ctypes.byref(nzl))
+        self.z0, self.nz = z0.value, nzl.value
+        self.shape = (5, self.nz, ny, nx)
+
+    def _check(self, rc):
+        if rc != 0:
+            raise OsbliError(rc, self._L.osbli_last_error(self._h).decode())
+
+    def set_stream(self, stream_handle: int | None):
+        self._check(self._L.osbli_set_stream(self._h, ctypes.c_void_p(stream_handle or 0)))
+
+    def set_state(self, q):
+        if tuple(q.shape) != self.shape:
+            raise ValueError(f"state shape {tuple(q.shape)} != {self.shape}")
+        p, dev = _ptr(q)
+        self._check(self._L.osbli_set_state(self._h, ctypes.c_void_p(p), dev))
+
+    def get_state(self, out=None):
+        if out is None:
+            out = np.empty(self.shape, dtype=np.float64)
+        p, dev = _ptr(out)
+        self._check(self._L.osbli_get_state(self._h, ctypes.c_void_p(p), dev))
+        return out
+
+    def step(self, n: int = 1):
+        self._check(self._L.osbli_step(self._h, int(n)))
+
+    def residual(self, out=None):
+        if out is None:
+            out = np.empty(self.shape, dtype=np.float64)
+        p, dev = _ptr(out)
+        self._check(self._L.osbli_residual(self._h, ctypes.c_void_p(p), dev))
+        return out
+
+    def diagnostics(self) -> Diagnostics:
+        d = _Diag()
+        self._check(self._L.osbli_diagnostics(self._h, ctypes.byref(d)))
+        return Diagnostics(d.t, d.step, d.kinetic_energy, d.enstrophy, d.dissipation)
+
+    def sync(self):
+        self._check(self._L.osbli_sync(self._h))
+
+    @property
+    def kernel_launches(self) -> int:
+        return int(self._L.osbli_kernel_launches(self._h))
+
+    def close(self):
+        if self._h:
+            self._L.osbli_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+def inviscid() -> float:
+    return math.inf
