@@ -1,0 +1,309 @@
+"""Benchmark of the B200-native OpenSBLI hot path (one JSON line on rank 0).
+
+Metric (BASELINE.json): grid-point RK3 updates per second (fp64) — one update =
+one full 3-stage low-storage RK3 step of one grid point — and the fraction of
+the HBM roofline implied by the compulsory 400 B per point-step.
+
+Default workload (N=1): BASELINE configs[3], the north-star case — Taylor-Green
+vortex 256^3, 12th-order central differences, RK3, Re=1600, Pr=0.71, M=0.1,
+gamma=1.4, dt = 3.385e-3*64/256.  configs[1] (64^3, 4th order)
+fits in L2 and is a parity case.  N>1 (torchrun): weak scaling, 256^3 per GPU
+(global 256 x 256 x 256N, z-slab decomposition, NCCL ghost exchange).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl osbli|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "tgv256_o12": dict(n=256, order=12, scheme=1, desc="BASELINE configs[3]: TGV 256^3 12th order RK3"),
+    "tgv256_o8": dict(n=256, order=8, scheme=1, desc="BASELINE configs[4]: TGV 256^3/GPU 8th order RK3"),
+    "tgv64_o4": dict(n=64, order=4, scheme=1, desc="BASELINE configs[1]: TGV 64^3 4th order RK3"),
+}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,"
+                 "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.out = self.proc.communicate(timeout=5)[0]
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                self.out = ""
+        else:
+            self.out = ""
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def oracle_rate(order: int, dx: float, dt: float, budget_s: float, min_steps: int = 1):
+    """Oracle (single-threaded C++) RK3 throughput on a bounded sample: a periodic
+    24^3 grid at the workload's spacing, order, time step and TGV state."""
+    from inputs import TGV_PHYS, tgv
+    from oracle import core
+    n = 24
+    p = core.OracleParams(n, n, n, order, dx, dt=dt, **TGV_PHYS)
+    Q = tgv(n, n, n, dx=dx)
+    t0 = time.perf_counter()
+    steps = 0
+    while steps < min_steps or time.perf_counter() - t0 < budget_s:
+        Q = core.step(p, Q, 1, 1)
+        steps += 1
+    el = time.perf_counter() - t0
+    return n ** 3 * steps / el, steps, el, f"oracle RK3 on a periodic 24^3 TGV sample at the workload's dx/order/dt, {steps} steps, {el:.1f} s"
+
+
+def run_reference(args, cfg, n_glob, dx, dt):
+    """--impl reference: the oracle (this tier's reference arm), rank 0 only.
+    W untimed + exactly K timed oracle RK3 steps, each on the bounded 24^3 sample."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from inputs import TGV_PHYS, tgv
+    from oracle import core
+    ns = 24
+    p = core.OracleParams(ns, ns, ns, cfg["order"], dx, dt=dt, **TGV_PHYS)
+    Q = tgv(ns, ns, ns, dx=dx)
+    for _ in range(args.warmup):
+        Q = core.step(p, Q, 1, 1)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        Q = core.step(p, Q, 1, 1)
+    el = time.perf_counter() - t0
+    rate = ns ** 3 * args.steps / el
+    sample = (f"oracle RK3 on a periodic {ns}^3 TGV sample at the workload's dx/order/dt "
+              f"(per-point work identical to the {n_glob}^3 grid), {args.steps} steps, {el:.1f} s")
+    line = {
+        "impl": "reference", "metric": "grid-point RK3 updates/s (fp64)", "value": rate,
+        "unit": "pt-steps/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg["desc"], "grid": [n_glob] * 3, "order": cfg["order"]},
+        "cpu_baseline": {"value": rate, "unit": "pt-steps/s", "cores": 1, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": rate, "unit": "pt-steps/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="osbli", choices=["osbli", "reference"])
+    ap.add_argument("--config", default="tgv256_o12", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    cfg = CONFIGS[args.config]
+    n = cfg["n"]
+    dx = 2 * math.pi / n
+    dt = 3.385e-3 * 64 / n
+    if args.impl == "reference":
+        run_reference(args, cfg, n, dx, dt)
+        return
+
+    import numpy as np
+    import torch
+
+    import paper_1609_01277_b200 as osbli
+    from inputs import TGV_PHYS, tgv
+    from paper_1609_01277_b200 import perfmodel
+
+    rank, world, local, uid = osbli.init_distributed()
+    torch.cuda.set_device(local)
+    nz_glob = n * world  # weak scaling: 256^3 per GPU, TGV periods tiled in z
+    solver = osbli.Solver(n, n, nz_glob, cfg["order"], dx, dt, scheme=cfg["scheme"], rank=rank,
+                          nranks=world, unique_id=uid, **TGV_PHYS)
+    stream = torch.cuda.Stream()
+    solver.set_stream(stream.cuda_stream)
+    # input: this rank's slab of the global TGV, generated on the host, copied in
+    Qfull = tgv(n, n, solver.nz, dx=dx) if world == 1 else None
+    if Qfull is None:
+        import numpy as _np
+        z = (_np.arange(solver.nz) + solver.z0) * dx
+        from inputs.generators import conservative
+        Y, X = _np.meshgrid(_np.arange(n) * dx, _np.arange(n) * dx, indexing="ij")
+        Z = z[:, None, None]
+        g, M = TGV_PHYS["gamma"], TGV_PHYS["Minf"]
+        u0 = _np.sin(X) * _np.cos(Y) * _np.cos(Z)
+        u1 = -_np.cos(X) * _np.sin(Y) * _np.cos(Z)
+        p = 1 / (g * M * M) + (_np.cos(2 * X) + _np.cos(2 * Y)) * (2 + _np.cos(2 * Z)) / 16
+        Qfull = conservative(g * M * M * p, u0, u1, 0 * u0, p, g)
+    solver.set_state(Qfull)
+    npts_local = n * n * solver.nz
+    npts_glob = n * n * nz_glob
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    # warm-up
+    for _ in range(args.warmup):
+        solver.step(1)
+    solver.sync()
+
+    # ---- timed region: K steps, device-timed with CUDA events on the solver stream
+    launches0 = solver.kernel_launches
+    solver.set_kernel_timing(True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            solver.step(1)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    launches = solver.kernel_launches - launches0
+    ms = ev0.elapsed_time(ev1)
+    zms, xyms, nzl, nxyl = solver.kernel_timing()
+    solver.set_kernel_timing(False)
+    solver.sync()
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    value = npts_glob * args.steps / (ms * 1e-3)
+    ms_per_step = ms / args.steps
+
+    # ---- end to end through the public API with host buffers (pinned)
+    qh = torch.from_numpy(np.ascontiguousarray(Qfull)).pin_memory()
+    qo = torch.empty_like(qh).pin_memory()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(args.e2e_steps):
+        solver.set_state(qh)          # H2D of the step's input
+        solver.step(1)
+        solver.get_state(qo)          # D2H of the step's result
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = npts_glob * args.e2e_steps / (e2e_ms * 1e-3)
+    state_bytes = 5 * 8 * npts_local
+
+    if rank != 0:
+        return
+    peaks, peak_src = measured_peaks()
+    hbm = float(peaks["hbm_gbs"])
+    m = cfg["order"] // 2
+    # dominant kernel: the one with the larger share of the timed step
+    zflop, xyflop = perfmodel.flops(m)
+    zb, xyb = perfmodel.step_kernel_bytes(cfg["scheme"])
+    clocks = clk.summary()
+    fmax = float(peaks.get("sm_max_mhz", 1965.0))
+    fp64_peak = 148 * 64 * 2 * fmax * 1e6 / 1e12  # TFLOP/s: 148 SMs x 64 FP64 FMA lanes x 2
+    per_launch_pts = npts_local
+    z_avg = zms / max(nzl, 1)
+    xy_avg = xyms / max(nxyl, 1)
+    dom = "xypass" if xyms >= zms else "zpass"
+    avg = xy_avg if dom == "xypass" else z_avg
+    fl = xyflop if dom == "xypass" else zflop
+    achieved_tf = fl * per_launch_pts / (avg * 1e-3) / 1e12
+    roof = {
+        "kernel": dom, "bound": "alu", "achieved": achieved_tf, "peak": fp64_peak,
+        "unit": "TFLOP/s", "frac": achieved_tf / fp64_peak, "traffic": None,
+        "peak_source": f"FP64 = 148 SMs x 64 lanes x 2 flop x {fmax:.0f} MHz (guide unit counts; DESIGN.md §5)",
+        "flops_per_point": fl, "avg_launch_ms": avg,
+        "share_of_step": (xyms if dom == "xypass" else zms) / ms if ms > 0 else None,
+        "other_kernel": {"name": "zpass" if dom == "xypass" else "xypass",
+                         "avg_launch_ms": z_avg if dom == "xypass" else xy_avg,
+                         "achieved_tflops": (zflop if dom == "xypass" else xyflop) * per_launch_pts
+                         / ((z_avg if dom == "xypass" else xy_avg) * 1e-3) / 1e12},
+        "kernel_bytes_per_point_step": {"zpass": zb, "xypass": xyb},
+        "achieved_gbs": {"zpass": zb / 3 * per_launch_pts / (z_avg * 1e-3) / 1e9,
+                         "xypass": xyb / 3 * per_launch_pts / (xy_avg * 1e-3) / 1e9},
+    }
+    hbm_frac = value / world * perfmodel.COMPULSORY_BYTES_RK3 / (hbm * 1e9)
+    line = {
+        "metric": "grid-point RK3 updates/s (fp64)", "value": value, "unit": "pt-steps/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": cfg["desc"], "grid": [n, n, nz_glob], "order": cfg["order"],
+                   "scheme": "rk3", "Re": 1600.0, "dt": dt,
+                   "l2": "inputs larger than L2 (state 5 x 8 B x %d pts = %.0f MB per field-set)"
+                   % (npts_local, state_bytes / 1e6),
+                   "parallelism": f"z-slab x{world}"},
+        "hbm_roofline_frac": hbm_frac,
+        "hbm_roofline": {"compulsory_bytes_per_point_step": perfmodel.COMPULSORY_BYTES_RK3,
+                         "peak_gbs": hbm, "peak_source": peak_src},
+        "roofline": roof,
+        "clocks": clocks,
+        "gpu_launches": launches,
+        "e2e": {"value": e2e_value, "unit": "pt-steps/s", "h2d_bytes_per_step": state_bytes,
+                "d2h_bytes_per_step": state_bytes, "steps": args.e2e_steps},
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        rate, steps, el, sample = oracle_rate(cfg["order"], dx, dt, budget_s=15.0)
+        line["cpu_baseline"] = {"value": rate, "unit": "pt-steps/s", "cores": 1, "kind": "oracle",
+                                "sample": sample}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

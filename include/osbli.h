@@ -119,6 +119,14 @@ int osbli_residual(osbli_ctx *h, double *R, int on_device);
 /* Wait for queued work; surfaces asynchronous errors (NONFINITE, CUDA). */
 int osbli_sync(osbli_ctx *h);
 
+/* Instrumentation.  When enabled, osbli_step brackets every z-pass and xy-pass
+ * launch with CUDA events on the handle's stream; osbli_kernel_timing waits for
+ * them and returns the summed durations (ms) and launch counts since the last
+ * call (then resets).  Disabled by default. */
+int osbli_set_kernel_timing(osbli_ctx *h, int enable);
+int osbli_kernel_timing(osbli_ctx *h, double *zpass_ms, double *xypass_ms, long long *n_zpass,
+                        long long *n_xypass);
+
 /* Number of kernels this handle launched since creation (instrumentation). */
 long long osbli_kernel_launches(const osbli_ctx *h);
 

@@ -40,6 +40,10 @@ struct osbli_ctx {
   std::string err;
   ncclComm_t comm = nullptr;
   KParams base{};
+  // kernel timing instrumentation: events[3*i..3*i+2] bracket stage i's two kernels
+  bool timing = false;
+  std::vector<cudaEvent_t> events;
+  size_t ev_used = 0;
 };
 
 namespace {
@@ -392,8 +396,24 @@ int osbli_step(osbli_ctx *h, int n) {
       double *qin = h->b.q[h->cur], *qout = h->b.q[h->cur ^ 1];
       int r = exchange_ghosts(h, qin);
       if (r) return r;
-      CK(h, osbli::launch_stage(p, qin, qout, h->b.w, h->b.rz, h->b.gz, nullptr, h->b.flag,
-                                h->stream, &h->launches));
+      cudaEvent_t *ev = nullptr;
+      if (h->timing) {
+        if (h->ev_used + 3 > h->events.size()) {
+          for (int k = 0; k < 3; ++k) {
+            cudaEvent_t e;
+            CK(h, cudaEventCreate(&e));
+            h->events.push_back(e);
+          }
+        }
+        ev = &h->events[h->ev_used];
+        h->ev_used += 3;
+        CK(h, cudaEventRecord(ev[0], h->stream));
+      }
+      CK(h, osbli::launch_zpass(p, qin, h->b.rz, h->b.gz, 0, h->nz, h->stream, &h->launches));
+      if (ev) CK(h, cudaEventRecord(ev[1], h->stream));
+      CK(h, osbli::launch_xypass(p, qin, qout, h->b.w, h->b.rz, h->b.gz, nullptr, h->b.flag, 0,
+                                 h->nz, h->stream, &h->launches));
+      if (ev) CK(h, cudaEventRecord(ev[2], h->stream));
       h->cur ^= 1;
     }
     ++h->step_count;
@@ -479,6 +499,35 @@ int osbli_sync(osbli_ctx *h) {
 
 long long osbli_kernel_launches(const osbli_ctx *h) { return h ? h->launches : -1; }
 
+int osbli_set_kernel_timing(osbli_ctx *h, int enable) {
+  int u = check_usable(h);
+  if (u) return u;
+  h->timing = enable != 0;
+  h->ev_used = 0;
+  return OSBLI_OK;
+}
+
+int osbli_kernel_timing(osbli_ctx *h, double *zpass_ms, double *xypass_ms, long long *n_zpass,
+                        long long *n_xypass) {
+  int u = check_usable(h);
+  if (u) return u;
+  if (!zpass_ms || !xypass_ms || !n_zpass || !n_xypass) return fail(h, OSBLI_E_INVAL, "null output");
+  CK(h, cudaStreamSynchronize(h->stream));
+  double zs = 0.0, xs = 0.0;
+  for (size_t i = 0; i + 3 <= h->ev_used; i += 3) {
+    float a = 0.f, b = 0.f;
+    CK(h, cudaEventElapsedTime(&a, h->events[i], h->events[i + 1]));
+    CK(h, cudaEventElapsedTime(&b, h->events[i + 1], h->events[i + 2]));
+    zs += a;
+    xs += b;
+  }
+  *zpass_ms = zs;
+  *xypass_ms = xs;
+  *n_zpass = *n_xypass = (long long)(h->ev_used / 3);
+  h->ev_used = 0;
+  return OSBLI_OK;
+}
+
 const char *osbli_last_error(const osbli_ctx *h) {
   return h ? h->err.c_str() : g_create_error.c_str();
 }
@@ -487,6 +536,7 @@ void osbli_destroy(osbli_ctx *h) {
   if (!h) return;
   if (h->stream) cudaStreamSynchronize(h->stream);
   if (h->comm) ncclCommDestroy(h->comm);
+  for (auto e : h->events) cudaEventDestroy(e);
   free_all(h);
   if (h->own_stream) cudaStreamDestroy(h->own_stream);
   delete h;

@@ -230,11 +230,13 @@ __device__ __forceinline__ double d1prod(const KParams &p, const double *f, cons
 #pragma unroll
   for (int k = 1; k <= M; ++k) {
     const int cp = c + k * STRIDE, cm = c - k * STRIDE;
-    double vp = alpha * f[cp] * h[cp];
-    double vm = alpha * f[cm] * h[cm];
+    // products rounded explicitly (no FMA contraction across the two taps) so
+    // that a uniform state cancels exactly (R == 0, SURVEY §8(c) equilibrium pin)
+    double vp = __dmul_rn(__dmul_rn(alpha, f[cp]), h[cp]);
+    double vm = __dmul_rn(__dmul_rn(alpha, f[cm]), h[cm]);
     if (add) {
-      vp += add[cp];
-      vm += add[cm];
+      vp = __dadd_rn(vp, add[cp]);
+      vm = __dadd_rn(vm, add[cm]);
     }
     s = fma(p.a[k - 1], vp - vm, s);
   }
@@ -348,9 +350,13 @@ __global__ void __launch_bounds__(XY_THREADS, 2)
 #pragma unroll
     for (int k = 1; k <= M; ++k) {
       const int cp = c + k, cm = c - k;
-      dGx = fma(p.a[k - 1], (0.5 * Se[cp] + Sp[cp]) * Su0[cp] - (0.5 * Se[cm] + Sp[cm]) * Su0[cm], dGx);
+      const double gxp = __dmul_rn(fma(0.5, Se[cp], Sp[cp]), Su0[cp]);
+      const double gxm = __dmul_rn(fma(0.5, Se[cm], Sp[cm]), Su0[cm]);
+      dGx = fma(p.a[k - 1], gxp - gxm, dGx);
       const int dp = c + k * HX, dm = c - k * HX;
-      dGy = fma(p.a[k - 1], (0.5 * Se[dp] + Sp[dp]) * Su1[dp] - (0.5 * Se[dm] + Sp[dm]) * Su1[dm], dGy);
+      const double gyp = __dmul_rn(fma(0.5, Se[dp], Sp[dp]), Su1[dp]);
+      const double gym = __dmul_rn(fma(0.5, Se[dm], Sp[dm]), Su1[dm]);
+      dGy = fma(p.a[k - 1], gyp - gym, dGy);
     }
     const double heat = p.kappa * (d2s<M, 1>(p, ST, c) + d2s<M, HX>(p, ST, c));
     const double th = th_xy + g22;

@@ -67,6 +67,10 @@ def load():
     L.osbli_diagnostics.argtypes = [H, ctypes.POINTER(_Diag)]
     L.osbli_residual.argtypes = [H, vp, c_int]
     L.osbli_sync.argtypes = [H]
+    L.osbli_set_kernel_timing.argtypes = [H, c_int]
+    L.osbli_kernel_timing.argtypes = [H, ctypes.POINTER(c_double), ctypes.POINTER(c_double),
+                                      ctypes.POINTER(ctypes.c_longlong),
+                                      ctypes.POINTER(ctypes.c_longlong)]
     L.osbli_kernel_launches.argtypes = [H]
     L.osbli_kernel_launches.restype = ctypes.c_longlong
     L.osbli_last_error.argtypes = [H]
@@ -173,6 +177,17 @@ class Solver:
 
     def sync(self):
         self._check(self._L.osbli_sync(self._h))
+
+    def set_kernel_timing(self, enable: bool):
+        self._check(self._L.osbli_set_kernel_timing(self._h, 1 if enable else 0))
+
+    def kernel_timing(self):
+        """(zpass_ms_total, xypass_ms_total, n_zpass, n_xypass) since the last call."""
+        z, x = ctypes.c_double(), ctypes.c_double()
+        nz, nx = ctypes.c_longlong(), ctypes.c_longlong()
+        self._check(self._L.osbli_kernel_timing(self._h, ctypes.byref(z), ctypes.byref(x),
+                                                ctypes.byref(nz), ctypes.byref(nx)))
+        return z.value, x.value, nz.value, nx.value
 
     @property
     def kernel_launches(self) -> int:
