@@ -54,7 +54,7 @@ class ClockSampler:
                 ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,"
                  "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
                  "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "100"],
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
@@ -144,7 +144,7 @@ def run_reference(args, cfg, n_glob, dx, dt):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="osbli", choices=["osbli", "reference"])
     ap.add_argument("--config", default="tgv256_o12", choices=sorted(CONFIGS))
@@ -195,16 +195,19 @@ def main():
         if world > 1:
             torch.distributed.barrier()
 
-    # warm-up
-    for _ in range(args.warmup):
-        solver.step(1)
-    solver.sync()
-
-    # ---- timed region: K steps, device-timed with CUDA events on the solver stream
-    launches0 = solver.kernel_launches
-    solver.set_kernel_timing(True)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(torch.cuda.current_device()) as clk:
+        # warm-up (also covers nvidia-smi start-up so that samples land in the timed region)
+        t_w = time.perf_counter()
+        while True:
+            for _ in range(args.warmup):
+                solver.step(1)
+            solver.sync()
+            if time.perf_counter() - t_w > 1.0:
+                break
+        # ---- timed region: K steps, device-timed with CUDA events on the solver stream
+        launches0 = solver.kernel_launches
+        solver.set_kernel_timing(True)
         barrier()
         torch.cuda.synchronize()
         ev0.record(stream)

@@ -91,34 +91,51 @@ __global__ void __launch_bounds__(ZP_THREADS, 1)
   const int z0 = z_begin + blockIdx.z * ZP_TZ;
   const size_t FS = (size_t)p.nx * p.ny;
 
-  // ---- stage the z-stencil operands of NP planes x 32 columns (formulas)
-  for (int idx = threadIdx.x; idx < NP * 32; idx += ZP_THREADS) {
-    const int pl = idx >> 5, c = idx & 31;
-    int x = x0 + c;
-    if (x >= p.nx) x = wrapi(x, p.nx);
-    const int z = zread(p, z0 - M + pl);
-    const double *qp = q + qplane(p, z) + (size_t)y * p.nx + x;
-    const double rho = qp[0], m0 = qp[FS], m1 = qp[2 * FS], m2 = qp[3 * FS], e = qp[4 * FS];
-    const double r = 1.0 / rho;
-    const double u0 = m0 * r, u1 = m1 * r, u2 = m2 * r;
-    const double pr = p.gm1 * (e - 0.5 * (m0 * u0 + m1 * u1 + m2 * u2));
-    const double T = p.gM2 * pr * r;
-    double *s = S + pl * 32 + c;
-    s[ZS_RHO * NP * 32] = rho;
-    s[ZS_M0 * NP * 32] = m0;
-    s[ZS_M1 * NP * 32] = m1;
-    s[ZS_M2 * NP * 32] = m2;
-    s[ZS_E * NP * 32] = e;
-    s[ZS_U0 * NP * 32] = u0;
-    s[ZS_U1 * NP * 32] = u1;
-    s[ZS_U2 * NP * 32] = u2;
-    s[ZS_T * NP * 32] = T;
-    // momentum flux F_i2 = 1/2 m_i u_2 + delta_i2 p  (skew half + pressure)
-    s[ZS_F0 * NP * 32] = 0.5 * m0 * u2;
-    s[ZS_F1 * NP * 32] = 0.5 * m1 * u2;
-    s[ZS_F2 * NP * 32] = 0.5 * m2 * u2 + pr;
-    // energy flux G_2 = (1/2 e + p) u_2  (skew half + pressure work)
-    s[ZS_G * NP * 32] = (0.5 * e + pr) * u2;
+  // ---- stage the z-stencil operands of NP planes x 32 columns (formulas);
+  //      all global loads of a thread are issued before the first shared store
+  constexpr int NIT = (NP * 32 + ZP_THREADS - 1) / ZP_THREADS;
+  double raw[NIT][5];
+#pragma unroll
+  for (int it = 0; it < NIT; ++it) {
+    const int idx = threadIdx.x + it * ZP_THREADS;
+    if (idx < NP * 32) {
+      const int pl = idx >> 5, c = idx & 31;
+      int x = x0 + c;
+      if (x >= p.nx) x = wrapi(x, p.nx);
+      const int z = zread(p, z0 - M + pl);
+      const double *qp = q + qplane(p, z) + (size_t)y * p.nx + x;
+#pragma unroll
+      for (int f = 0; f < 5; ++f) raw[it][f] = __ldg(qp + f * FS);
+    }
+  }
+#pragma unroll
+  for (int it = 0; it < NIT; ++it) {
+    const int idx = threadIdx.x + it * ZP_THREADS;
+    if (idx < NP * 32) {
+      const int pl = idx >> 5, c = idx & 31;
+      const double rho = raw[it][0], m0 = raw[it][1], m1 = raw[it][2], m2 = raw[it][3],
+                   e = raw[it][4];
+      const double r = 1.0 / rho;
+      const double u0 = m0 * r, u1 = m1 * r, u2 = m2 * r;
+      const double pr = p.gm1 * (e - 0.5 * (m0 * u0 + m1 * u1 + m2 * u2));
+      const double T = p.gM2 * pr * r;
+      double *s = S + pl * 32 + c;
+      s[ZS_RHO * NP * 32] = rho;
+      s[ZS_M0 * NP * 32] = m0;
+      s[ZS_M1 * NP * 32] = m1;
+      s[ZS_M2 * NP * 32] = m2;
+      s[ZS_E * NP * 32] = e;
+      s[ZS_U0 * NP * 32] = u0;
+      s[ZS_U1 * NP * 32] = u1;
+      s[ZS_U2 * NP * 32] = u2;
+      s[ZS_T * NP * 32] = T;
+      // momentum flux F_i2 = 1/2 m_i u_2 + delta_i2 p  (skew half + pressure)
+      s[ZS_F0 * NP * 32] = 0.5 * m0 * u2;
+      s[ZS_F1 * NP * 32] = 0.5 * m1 * u2;
+      s[ZS_F2 * NP * 32] = 0.5 * m2 * u2 + pr;
+      // energy flux G_2 = (1/2 e + p) u_2  (skew half + pressure work)
+      s[ZS_G * NP * 32] = (0.5 * e + pr) * u2;
+    }
   }
   __syncthreads();
 
@@ -191,206 +208,7 @@ __global__ void __launch_bounds__(ZP_THREADS, 1)
   }
 }
 
-// ------------------------------------------------------------------ xy-pass
-constexpr int XY_TX = 32;
-constexpr int XY_TY = 8;
-constexpr int XY_THREADS = XY_TX * XY_TY;  // 256
-constexpr int XY_NF = 13;
-enum { XS_RHO = 0, XS_M0, XS_M1, XS_M2, XS_E, XS_U0, XS_U1, XS_U2, XS_P, XS_T, XS_G02, XS_G12, XS_G22 };
-
-template <int M>
-constexpr int xy_smem_bytes() {
-  return (XY_NF * (XY_TX + 2 * M) * (XY_TY + 2 * M) + 2 * XY_TX * (XY_TY + 2 * M)) *
-         (int)sizeof(double);
-}
-
-template <int M, int STRIDE>
-__device__ __forceinline__ double d1s(const KParams &p, const double *f, int c) {
-  double s = 0.0;
-#pragma unroll
-  for (int k = 1; k <= M; ++k) s = fma(p.a[k - 1], f[c + k * STRIDE] - f[c - k * STRIDE], s);
-  return s;
-}
-
-template <int M, int STRIDE>
-__device__ __forceinline__ double d2s(const KParams &p, const double *f, int c) {
-  const double f0 = f[c];
-  double s = 0.0;
-#pragma unroll
-  for (int k = 1; k <= M; ++k)
-    s = fma(p.b[k], (f[c + k * STRIDE] - f0) + (f[c - k * STRIDE] - f0), s);
-  return s;
-}
-
-// first derivative of the product (alpha * f * h + beta * e), taps from smem
-template <int M, int STRIDE>
-__device__ __forceinline__ double d1prod(const KParams &p, const double *f, const double *h,
-                                         const double *add, double alpha, int c) {
-  double s = 0.0;
-#pragma unroll
-  for (int k = 1; k <= M; ++k) {
-    const int cp = c + k * STRIDE, cm = c - k * STRIDE;
-    // products rounded explicitly (no FMA contraction across the two taps) so
-    // that a uniform state cancels exactly (R == 0, SURVEY §8(c) equilibrium pin)
-    double vp = __dmul_rn(__dmul_rn(alpha, f[cp]), h[cp]);
-    double vm = __dmul_rn(__dmul_rn(alpha, f[cm]), h[cm]);
-    if (add) {
-      vp = __dadd_rn(vp, add[cp]);
-      vm = __dadd_rn(vm, add[cm]);
-    }
-    s = fma(p.a[k - 1], vp - vm, s);
-  }
-  return s;
-}
-
-template <int M>
-__global__ void __launch_bounds__(XY_THREADS, 2)
-    xypass_kernel(const KParams p, const double *__restrict__ q, double *__restrict__ qout,
-                  double *__restrict__ w, const double *__restrict__ rz,
-                  const double *__restrict__ gz, double *__restrict__ rout,
-                  unsigned int *__restrict__ flag, int z_begin) {
-  constexpr int HX = XY_TX + 2 * M, HY = XY_TY + 2 * M, HN = HX * HY;
-  extern __shared__ double S[];
-  double *E = S + XY_NF * HN;  // [2][HY][32]: g00, g10 on the y-extended tile
-  const int z = z_begin + blockIdx.z;
-  const int x0 = blockIdx.x * XY_TX, y0 = blockIdx.y * XY_TY;
-  const size_t FS = (size_t)p.nx * p.ny;
-  const double *qp = q + qplane(p, z);
-  const double *gp = gz + (size_t)z * 3 * FS;
-
-  // ---- stage tile + halo (formulas; EOS P:259-266)
-  for (int idx = threadIdx.x; idx < HN; idx += XY_THREADS) {
-    const int hx = idx % HX, hy = idx / HX;
-    const int x = wrapi(x0 - M + hx, p.nx), y = wrapi(y0 - M + hy, p.ny);
-    const size_t off = (size_t)y * p.nx + x;
-    const double rho = qp[off], m0 = qp[FS + off], m1 = qp[2 * FS + off], m2 = qp[3 * FS + off],
-                 e = qp[4 * FS + off];
-    const double r = 1.0 / rho;
-    const double u0 = m0 * r, u1 = m1 * r, u2 = m2 * r;
-    const double pr = p.gm1 * (e - 0.5 * (m0 * u0 + m1 * u1 + m2 * u2));
-    S[XS_RHO * HN + idx] = rho;
-    S[XS_M0 * HN + idx] = m0;
-    S[XS_M1 * HN + idx] = m1;
-    S[XS_M2 * HN + idx] = m2;
-    S[XS_E * HN + idx] = e;
-    S[XS_U0 * HN + idx] = u0;
-    S[XS_U1 * HN + idx] = u1;
-    S[XS_U2 * HN + idx] = u2;
-    S[XS_P * HN + idx] = pr;
-    S[XS_T * HN + idx] = p.gM2 * pr * r;
-    S[XS_G02 * HN + idx] = gp[off];
-    S[XS_G12 * HN + idx] = gp[FS + off];
-    S[XS_G22 * HN + idx] = gp[2 * FS + off];
-  }
-  __syncthreads();
-  // ---- inner derivatives g00 = D_x u0, g10 = D_x u1 on the y-extended tile
-  //      (the nested derivatives D_y g00, D_y g10)
-  for (int idx = threadIdx.x; idx < XY_TX * HY; idx += XY_THREADS) {
-    const int tx = idx & 31, hy = idx >> 5;
-    const int c = hy * HX + tx + M;
-    E[idx] = d1s<M, 1>(p, S + XS_U0 * HN, c);
-    E[XY_TX * HY + idx] = d1s<M, 1>(p, S + XS_U1 * HN, c);
-  }
-  __syncthreads();
-
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const int c = (ty + M) * HX + tx + M;
-  const int ce = (ty + M) * XY_TX + tx;
-  const double *Srho = S + XS_RHO * HN, *Sm0 = S + XS_M0 * HN, *Sm1 = S + XS_M1 * HN,
-               *Sm2 = S + XS_M2 * HN, *Se = S + XS_E * HN, *Su0 = S + XS_U0 * HN,
-               *Su1 = S + XS_U1 * HN, *Su2 = S + XS_U2 * HN, *Sp = S + XS_P * HN,
-               *ST = S + XS_T * HN;
-  const double rho = Srho[c], m0 = Sm0[c], m1 = Sm1[c], m2 = Sm2[c], e = Se[c];
-  const double u0 = Su0[c], u1 = Su1[c], u2 = Su2[c];
-  const double g02 = S[XS_G02 * HN + c], g12 = S[XS_G12 * HN + c], g22 = S[XS_G22 * HN + c];
-
-  // ---- velocity gradients and viscous terms
-  const double g00 = d1s<M, 1>(p, Su0, c), g10 = d1s<M, 1>(p, Su1, c), g20 = d1s<M, 1>(p, Su2, c);
-  const double g01 = d1s<M, HX>(p, Su0, c), g11 = d1s<M, HX>(p, Su1, c), g21 = d1s<M, HX>(p, Su2, c);
-  const double d00u0 = d2s<M, 1>(p, Su0, c), d11u0 = d2s<M, HX>(p, Su0, c);
-  const double d00u1 = d2s<M, 1>(p, Su1, c), d11u1 = d2s<M, HX>(p, Su1, c);
-  const double d00u2 = d2s<M, 1>(p, Su2, c), d11u2 = d2s<M, HX>(p, Su2, c);
-  // mixed (commuted, D-7): D_x g11 -> D_y g10 ; D_y g00 ; D_x g22 ; D_y g22 ;
-  // D_z g00 -> D_x g02 ; D_z g11 -> D_y g12
-  const double dy_g10 = d1s<M, XY_TX>(p, E + XY_TX * HY, ce);
-  const double dy_g00 = d1s<M, XY_TX>(p, E, ce);
-  const double dx_g22 = d1s<M, 1>(p, S + XS_G22 * HN, c);
-  const double dy_g22 = d1s<M, HX>(p, S + XS_G22 * HN, c);
-  const double dx_g02 = d1s<M, 1>(p, S + XS_G02 * HN, c);
-  const double dy_g12 = d1s<M, HX>(p, S + XS_G12 * HN, c);
-  const double third = 1.0 / 3.0;
-  // V_i (x,y parts) = nu [ D_xx u_i + D_yy u_i + 1/3 ( D_ii u_i + sum_{j != i} D_i D_j u_j ) ]
-  const double V0 = p.nu * (d00u0 + d11u0 + third * (d00u0 + dy_g10 + dx_g22));
-  const double V1 = p.nu * (d00u1 + d11u1 + third * (d11u1 + dy_g00 + dy_g22));
-  const double V2 = p.nu * (d00u2 + d11u2 + third * (dx_g02 + dy_g12));
-
-  // ---- skew-symmetric convection, x and y parts
-  const double th_xy = g00 + g11;
-  double R[5];
-  {
-    const double drx = d1s<M, 1>(p, Srho, c), dry = d1s<M, HX>(p, Srho, c);
-    const double dm0x = d1s<M, 1>(p, Sm0, c), dm1y = d1s<M, HX>(p, Sm1, c);
-    R[0] = -0.5 * (dm0x + dm1y + u0 * drx + u1 * dry + rho * th_xy);
-  }
-  const double *Sm[3] = {Sm0, Sm1, Sm2};
-  const double mc[3] = {m0, m1, m2};
-  const double Vv[3] = {V0, V1, V2};
-#pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    const double dmx = d1s<M, 1>(p, Sm[i], c), dmy = d1s<M, HX>(p, Sm[i], c);
-    // F_i0 = 1/2 m_i u_0 + delta_i0 p ; F_i1 = 1/2 m_i u_1 + delta_i1 p
-    const double dFx = d1prod<M, 1>(p, Sm[i], Su0, i == 0 ? Sp : nullptr, 0.5, c);
-    const double dFy = d1prod<M, HX>(p, Sm[i], Su1, i == 1 ? Sp : nullptr, 0.5, c);
-    R[1 + i] = -(dFx + dFy + 0.5 * (u0 * dmx + u1 * dmy + mc[i] * th_xy)) + Vv[i];
-  }
-  {
-    const double dex = d1s<M, 1>(p, Se, c), dey = d1s<M, HX>(p, Se, c);
-    // G_j = (1/2 e + p) u_j
-    double dGx = 0.0, dGy = 0.0;
-#pragma unroll
-    for (int k = 1; k <= M; ++k) {
-      const int cp = c + k, cm = c - k;
-      const double gxp = __dmul_rn(fma(0.5, Se[cp], Sp[cp]), Su0[cp]);
-      const double gxm = __dmul_rn(fma(0.5, Se[cm], Sp[cm]), Su0[cm]);
-      dGx = fma(p.a[k - 1], gxp - gxm, dGx);
-      const int dp = c + k * HX, dm = c - k * HX;
-      const double gyp = __dmul_rn(fma(0.5, Se[dp], Sp[dp]), Su1[dp]);
-      const double gym = __dmul_rn(fma(0.5, Se[dm], Sp[dm]), Su1[dm]);
-      dGy = fma(p.a[k - 1], gyp - gym, dGy);
-    }
-    const double heat = p.kappa * (d2s<M, 1>(p, ST, c) + d2s<M, HX>(p, ST, c));
-    const double th = th_xy + g22;
-    const double s01 = g01 + g10, s02 = g02 + g20, s12 = g12 + g21;
-    // viscous dissipation tau_ij g_ij (eq. 8) = nu [2 sum g_ii^2 + sum_{i<j} (g_ij+g_ji)^2 - 2/3 th^2]
-    const double Phi = p.nu * (2.0 * (g00 * g00 + g11 * g11 + g22 * g22) + s01 * s01 + s02 * s02 +
-                               s12 * s12 - (2.0 / 3.0) * th * th);
-    R[4] = -(dGx + dGy + 0.5 * (u0 * dex + u1 * dey + e * th_xy)) + heat + Phi +
-           (u0 * V0 + u1 * V1 + u2 * V2);
-  }
-
-  // ---- epilogue: add the z-pass partial residual, RK stage update
-  const int x = x0 + tx, y = y0 + ty;
-  if (x >= p.nx || y >= p.ny) return;
-  const size_t o = (size_t)z * 5 * FS + (size_t)y * p.nx + x;
-  const double qc[5] = {rho, m0, m1, m2, e};
-  double *qo = qout ? qout + qplane(p, z) + (size_t)y * p.nx + x : nullptr;
-  bool bad = false;
-#pragma unroll
-  for (int f = 0; f < 5; ++f) {
-    const double Rf = R[f] + rz[o + f * FS];
-    if (rout) {
-      rout[o + f * FS] = Rf;
-      continue;
-    }
-    double wn = p.dt * Rf;
-    if (p.read_w) wn = fma(p.A, w[o + f * FS], wn);
-    if (p.write_w) w[o + f * FS] = wn;
-    const double qn = fma(p.B, wn, qc[f]);
-    qo[f * FS] = qn;
-    bad |= !isfinite(qn);
-  }
-  if (bad) atomicOr(flag, 1u);
-}
+#include "xypass.cuh"
 
 // ------------------------------------------------------------------ diagnostics
 __global__ void velocity_kernel(const KParams p, const double *__restrict__ q,
