@@ -8,7 +8,7 @@ LIB := $(PKG)/libosbli.so
 
 all: $(LIB) oracle/liboracle.so
 
-$(CSRC)/kernels.o: $(CSRC)/kernels.cu $(CSRC)/kernels.h
+$(CSRC)/kernels.o: $(CSRC)/kernels.cu $(CSRC)/kernels.h $(wildcard $(CSRC)/*.cuh)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(CSRC)/ptxas.log || (cat $(CSRC)/ptxas.log; false)
 
 $(CSRC)/api.o: $(CSRC)/api.cpp $(CSRC)/kernels.h include/osbli.h

@@ -32,14 +32,24 @@ struct XYGeom {
   static constexpr int NPT = TP * XY_TY;        // tile points (padded)
   static constexpr int EXT = TP * HY;           // g00 / g10 on the y-extended tile
   static constexpr int W = 4 + 2 * M;           // window length (RX = RY = 4)
-  // layout (doubles): fields | E0 | E1 | XA[5] | XB[5]
+  // layout (doubles): fields | E0 | E1 | XA[5] | XB[5] | PF[10] (prefetched Rz, W)
   static constexpr int OFF_E0 = XY_NF * FSZ;
   static constexpr int OFF_E1 = OFF_E0 + EXT;
   static constexpr int OFF_XA = OFF_E1 + EXT;
   static constexpr int OFF_XB = OFF_XA + 5 * NPT;
-  static constexpr int TOTAL = OFF_XB + 5 * NPT;
+  static constexpr int OFF_PF = OFF_XB + 5 * NPT;
+  static constexpr int TOTAL = OFF_PF + 10 * XY_TX * XY_TY;
   static constexpr int BYTES = TOTAL * (int)sizeof(double);
 };
+
+// 8-byte asynchronous global -> shared copy (LDGSTS), completed by cp_async_wait_all
+__device__ __forceinline__ void cp_async8(double *smem, const double *gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
 
 template <int M>
 constexpr int xy_smem_bytes() {
@@ -187,6 +197,24 @@ __global__ void __launch_bounds__(XY_THREADS, 1)
   const size_t FS = (size_t)p.nx * p.ny;
   const double *qp = q + qplane(p, z);
   const double *gp = gz + (size_t)z * 3 * FS;
+
+  // ---- prefetch the epilogue operands (z-pass partial residual Rz, RK register W)
+  //      asynchronously so that their latency hides behind phases X and Y
+  double *PF = S + Gm::OFF_PF;
+  for (int lin = tid; lin < XY_TX * XY_TY; lin += XY_THREADS) {
+    const int ty = lin / XY_TX, tx = lin - ty * XY_TX;
+    const int x = x0 + tx, y = y0 + ty;
+    if (x < p.nx && y < p.ny) {
+      const size_t o = (size_t)z * 5 * FS + (size_t)y * p.nx + x;
+#pragma unroll
+      for (int f = 0; f < 5; ++f) cp_async8(PF + f * XY_TX * XY_TY + lin, rz + o + f * FS);
+      if (p.read_w && !rout) {
+#pragma unroll
+        for (int f = 0; f < 5; ++f) cp_async8(PF + (5 + f) * XY_TX * XY_TY + lin, w + o + f * FS);
+      }
+    }
+  }
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
 
   // ---- stage the tile + halo: conservative state, p, 1/rho, g_i2.  All global
   //      loads of a thread are issued before the first shared store (MLP).
@@ -344,6 +372,8 @@ __global__ void __launch_bounds__(XY_THREADS, 1)
   __syncthreads();
 
   // ---- epilogue: R = A + B + Rz ; W <- A W + dt R ; Q' <- Q + B W  (coalesced rows)
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  __syncthreads();
   bool bad = false;
   for (int lin = tid; lin < XY_TX * XY_TY; lin += XY_THREADS) {
     const int ty = lin / XY_TX, tx = lin - ty * XY_TX;
@@ -356,13 +386,13 @@ __global__ void __launch_bounds__(XY_THREADS, 1)
     const int fidx[5] = {XF_RHO, XF_M0, XF_M1, XF_M2, XF_E};
 #pragma unroll
     for (int f = 0; f < 5; ++f) {
-      const double Rf = XA[f * NPT + pt] + XB[f * NPT + pt] + rz[o + f * FS];
+      const double Rf = XA[f * NPT + pt] + XB[f * NPT + pt] + PF[f * XY_TX * XY_TY + lin];
       if (rout) {
         rout[o + f * FS] = Rf;
         continue;
       }
       double wn = p.dt * Rf;
-      if (p.read_w) wn = fma(p.A, w[o + f * FS], wn);
+      if (p.read_w) wn = fma(p.A, PF[(5 + f) * XY_TX * XY_TY + lin], wn);
       if (p.write_w) w[o + f * FS] = wn;
       const double qn = fma(p.B, wn, S[fidx[f] * FSZ + c]);
       qo[f * FS] = qn;
