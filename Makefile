@@ -5,6 +5,16 @@ CSRC := $(PKG)/csrc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v
 LIB := $(PKG)/libosbli.so
+# NCCL: the copy torch loads (pip nvidia-nccl), so that one libnccl.so.2 serves
+# both torch and libosbli in a process regardless of import order
+NCCL_HOME ?= $(shell python -c "import nvidia.nccl as n; print(list(n.__path__)[0])" 2>/dev/null)
+ifneq ($(NCCL_HOME),)
+NCCL_INC := -I$(NCCL_HOME)/include
+NCCL_LIB := -L$(NCCL_HOME)/lib -l:libnccl.so.2 -Xlinker -rpath=$(NCCL_HOME)/lib
+else
+NCCL_INC :=
+NCCL_LIB := -lnccl
+endif
 
 all: $(LIB) oracle/liboracle.so
 
@@ -12,10 +22,10 @@ $(CSRC)/kernels.o: $(CSRC)/kernels.cu $(CSRC)/kernels.h $(wildcard $(CSRC)/*.cuh
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(CSRC)/ptxas.log || (cat $(CSRC)/ptxas.log; false)
 
 $(CSRC)/api.o: $(CSRC)/api.cpp $(CSRC)/kernels.h include/osbli.h
-	$(NVCC) $(ARCH) -O2 -std=c++17 -Xcompiler -fPIC -x cu -c $< -o $@
+	$(NVCC) $(ARCH) -O2 -std=c++17 -Xcompiler -fPIC $(NCCL_INC) -x cu -c $< -o $@
 
 $(LIB): $(CSRC)/kernels.o $(CSRC)/api.o
-	$(NVCC) $(ARCH) -shared -o $@ $^ -lnccl -lcudart
+	$(NVCC) $(ARCH) -shared -o $@ $^ $(NCCL_LIB) -lcudart
 
 oracle/liboracle.so: oracle/oracle.cpp
 	g++ -O2 -ffp-contract=off -fno-fast-math -std=c++17 -shared -fPIC $< -o $@

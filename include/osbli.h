@@ -93,6 +93,29 @@ int osbli_create_dist(int nx, int ny, int nz, int order, double dx, double dt, d
 /* Fill 128 bytes at id_out with a fresh ncclUniqueId (rank 0 only). */
 int osbli_nccl_unique_id(void *id_out);
 
+/* Host-only helpers of the slab decomposition (no device needed).
+ * osbli_slab_bounds: planes [*z0, *z0 + *nz_local) of `rank` when nz planes are
+ *   split over nranks (near-equal; the first nz % nranks ranks get one more).
+ * osbli_ghost_plan: the two ghost transfers of one stage, m planes each, in
+ *   local plane indices (interior 0..nz_local-1, ghosts -m..-1, nz_local..):
+ *   plan[4t+0] send peer, plan[4t+1] first plane sent, plan[4t+2] receive peer,
+ *   plan[4t+3] first ghost plane received, for t = 0, 1.  Every rank posts the
+ *   transfers in this order; rank r's transfer t send matches its peer's
+ *   transfer t receive. */
+int osbli_slab_bounds(int nz, int nranks, int rank, int *z0, int *nz_local);
+int osbli_ghost_plan(int rank, int nranks, int nz_local, int m, int *plan);
+
+/* Single-GPU test transport: create nslabs handles (out[0..nslabs-1]) that
+ * split nz exactly like osbli_create_dist and exchange ghost planes by device
+ * copies instead of NCCL, on one shared stream.  They run the distributed
+ * (ghost-plane) kernel path; advance them together with osbli_loopback_step
+ * (osbli_step on a member returns OSBLI_E_INVAL).  set_state/get_state/
+ * residual/diagnostics work per member (diagnostics gather all members). */
+int osbli_create_loopback(int nx, int ny, int nz, int order, double dx, double dt, double Re,
+                          double Pr, double Minf, double gamma, int scheme, int nslabs,
+                          osbli_ctx **out);
+int osbli_loopback_step(osbli_ctx **hs, int nslabs, int n);
+
 /* Slab owned by this rank: global planes [*z0, *z0 + *nz_local). */
 int osbli_local_box(const osbli_ctx *h, int *z0, int *nz_local);
 

@@ -11,12 +11,15 @@ as device pointers) and process groups (``init_distributed``).
 from .native import (  # noqa: F401
     OSBLI_EULER,
     OSBLI_RK3,
+    LoopbackGroup,
     OsbliError,
     Solver,
+    ghost_plan,
+    slab_bounds,
     build,
     lib_path,
     load,
     nccl_unique_id,
     version,
 )
-from .distributed import init_distributed, slab_bounds  # noqa: F401
+from .distributed import exchange_ghosts_torch, init_distributed  # noqa: F401

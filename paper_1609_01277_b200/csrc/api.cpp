@@ -23,6 +23,13 @@
 using osbli::Bufs;
 using osbli::KParams;
 
+struct LoopGroup {
+  std::vector<osbli_ctx *> members;
+  std::vector<cudaStream_t> streams;  // every member's own stream, destroyed with the group
+  int live = 0;
+};
+static std::vector<cudaStream_t> &g_loop_streams(LoopGroup *g) { return g->streams; }
+
 struct osbli_ctx {
   int nx = 0, ny = 0, nz_global = 0, nz = 0, z0 = 0, order = 0, m = 0, scheme = 0;
   int rank = 0, nranks = 1;
@@ -40,6 +47,8 @@ struct osbli_ctx {
   std::string err;
   ncclComm_t comm = nullptr;
   KParams base{};
+  // loopback transport (one GPU, several slabs): the group of sibling handles
+  struct LoopGroup *loop = nullptr;
   // kernel timing instrumentation: events[3*i..3*i+2] bracket stage i's two kernels
   bool timing = false;
   std::vector<cudaEvent_t> events;
@@ -211,25 +220,59 @@ int check_usable(osbli_ctx *h) {
   return OSBLI_OK;
 }
 
-// z ghost planes of Q buffer `q` from the neighbouring slabs (periodic ring).
+// Near-equal slab partition of nz planes over nranks (z-slab decomposition):
+// the first nz % nranks ranks own one extra plane.
+void slab_partition(int nz, int nranks, int rank, int *z0, int *nzl) {
+  const int base = nz / nranks, extra = nz % nranks;
+  *nzl = base + (rank < extra ? 1 : 0);
+  *z0 = rank * base + (rank < extra ? rank : extra);
+}
+
+// Ghost-plane exchange plan of one rank (periodic ring in z), m planes each:
+//   transfer 0: send local planes [0, m)           to the rank below,
+//               receive into ghost planes [nzl, nzl+m) from the rank above;
+//   transfer 1: send local planes [nzl-m, nzl)     to the rank above,
+//               receive into ghost planes [-m, 0)    from the rank below.
+// plan = {send_peer, send_plane, recv_peer, recv_plane} x 2 (local plane indices).
+void ghost_plan(int rank, int nranks, int nzl, int m, int plan[8]) {
+  const int up = (rank + 1) % nranks, dn = (rank - 1 + nranks) % nranks;
+  const int p[8] = {dn, 0, up, nzl, up, nzl - m, dn, -m};
+  for (int i = 0; i < 8; ++i) plan[i] = p[i];
+}
+
+// z ghost planes of Q buffer `q` from the neighbouring slabs, over NCCL
+// (one process per GPU) or by device copies between sibling handles
+// (loopback transport on one GPU).
 int exchange_ghosts(osbli_ctx *h, double *q) {
   if (h->nranks == 1) return OSBLI_OK;
   const int G = h->m;
-  const size_t FS = (size_t)h->nx * h->ny;
-  const size_t cnt = (size_t)G * 5 * FS;
-  const size_t plane = 5 * FS;
-  const int up = (h->rank + 1) % h->nranks, dn = (h->rank - 1 + h->nranks) % h->nranks;
-  double *interior_lo = q + (size_t)G * plane;          // planes [0, G)
-  double *interior_hi = q + (size_t)h->nz * plane;      // planes [nz-G, nz)
-  double *ghost_lo = q;                                 // planes [-G, 0)
-  double *ghost_hi = q + (size_t)(h->nz + G) * plane;   // planes [nz, nz+G)
-  NK(h, ncclGroupStart());
-  NK(h, ncclSend(interior_lo, cnt, ncclDouble, dn, h->comm, h->stream));
-  NK(h, ncclRecv(ghost_hi, cnt, ncclDouble, up, h->comm, h->stream));
-  NK(h, ncclSend(interior_hi, cnt, ncclDouble, up, h->comm, h->stream));
-  NK(h, ncclRecv(ghost_lo, cnt, ncclDouble, dn, h->comm, h->stream));
-  NK(h, ncclGroupEnd());
-  return OSBLI_OK;
+  const size_t plane = 5 * (size_t)h->nx * h->ny;
+  const size_t cnt = (size_t)G * plane;
+  int plan[8];
+  ghost_plan(h->rank, h->nranks, h->nz, G, plan);
+  auto at = [&](double *base, int local_plane) { return base + (size_t)(local_plane + G) * plane; };
+  if (h->comm) {
+    NK(h, ncclGroupStart());
+    for (int t = 0; t < 2; ++t) {
+      NK(h, ncclSend(at(q, plan[4 * t + 1]), cnt, ncclDouble, plan[4 * t + 0], h->comm, h->stream));
+      NK(h, ncclRecv(at(q, plan[4 * t + 3]), cnt, ncclDouble, plan[4 * t + 2], h->comm, h->stream));
+    }
+    NK(h, ncclGroupEnd());
+    return OSBLI_OK;
+  }
+  if (h->loop) {
+    // I receive what my peer sends under the same transfer index: for
+    // transfer t the source is peer plan[4t+2]'s plane given by ITS plan.
+    for (int t = 0; t < 2; ++t) {
+      osbli_ctx *src = h->loop->members[plan[4 * t + 2]];
+      int splan[8];
+      ghost_plan(src->rank, src->nranks, src->nz, G, splan);
+      CK(h, cudaMemcpyAsync(at(q, plan[4 * t + 3]), at(src->b.q[src->cur], splan[4 * t + 1]),
+                            cnt * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+    }
+    return OSBLI_OK;
+  }
+  return fail(h, OSBLI_E_STATE, "distributed handle without a transport");
 }
 
 int check_flag(osbli_ctx *h) {
@@ -291,10 +334,9 @@ int osbli_create_dist(int nx, int ny, int nz, int order, double dx, double dt, d
     return OSBLI_E_INVAL;
   }
   const int m = order / 2;
-  // near-equal slabs: the first (nz % nranks) ranks get one extra plane
+  int z0 = 0, nzl = 0;
+  slab_partition(nz, nranks, rank, &z0, &nzl);
   const int base = nz / nranks, extra = nz % nranks;
-  const int nzl = base + (rank < extra ? 1 : 0);
-  const int z0 = rank * base + (rank < extra ? rank : extra);
   if (nranks > 1 && base < m) {
     g_create_error = "every slab needs at least order/2 planes";
     return OSBLI_E_INVAL;
@@ -341,6 +383,7 @@ int osbli_local_box(const osbli_ctx *h, int *z0, int *nz_local) {
 int osbli_set_stream(osbli_ctx *h, void *cuda_stream) {
   int u = check_usable(h);
   if (u) return u;
+  if (h->loop) return fail(h, OSBLI_E_INVAL, "loopback slabs share the group stream");
   // order the switch: work queued on the old stream completes first
   CK(h, cudaStreamSynchronize(h->stream));
   h->stream = cuda_stream ? (cudaStream_t)cuda_stream : h->own_stream;
@@ -372,51 +415,148 @@ int osbli_get_state(osbli_ctx *h, double *q, int on_device) {
   return OSBLI_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+// One stage s of the time scheme on handle h: ghost exchange, z-pass, xy-pass.
+int run_stage(osbli_ctx *h, int s, bool exchange = true) {
+  static const double RK_A[3] = {0.0, -5.0 / 9.0, -153.0 / 128.0};
+  static const double RK_B[3] = {1.0 / 3.0, 15.0 / 16.0, 8.0 / 15.0};
+  KParams p = h->base;
+  if (h->scheme == OSBLI_RK3) {
+    p.A = RK_A[s];
+    p.B = RK_B[s];
+    p.read_w = (s > 0);
+    p.write_w = (s < 2);
+  } else {
+    p.A = 0.0;
+    p.B = 1.0;
+    p.read_w = 0;
+    p.write_w = 0;
+  }
+  double *qin = h->b.q[h->cur], *qout = h->b.q[h->cur ^ 1];
+  if (exchange) {
+    int r = exchange_ghosts(h, qin);
+    if (r) return r;
+  }
+  cudaEvent_t *ev = nullptr;
+  if (h->timing) {
+    if (h->ev_used + 3 > h->events.size()) {
+      for (int k = 0; k < 3; ++k) {
+        cudaEvent_t e;
+        CK(h, cudaEventCreate(&e));
+        h->events.push_back(e);
+      }
+    }
+    ev = &h->events[h->ev_used];
+    h->ev_used += 3;
+    CK(h, cudaEventRecord(ev[0], h->stream));
+  }
+  CK(h, osbli::launch_zpass(p, qin, h->b.rz, h->b.gz, 0, h->nz, h->stream, &h->launches));
+  if (ev) CK(h, cudaEventRecord(ev[1], h->stream));
+  CK(h, osbli::launch_xypass(p, qin, qout, h->b.w, h->b.rz, h->b.gz, nullptr, h->b.flag, 0, h->nz,
+                             h->stream, &h->launches));
+  if (ev) CK(h, cudaEventRecord(ev[2], h->stream));
+  h->cur ^= 1;
+  return OSBLI_OK;
+}
+
+int nstages(const osbli_ctx *h) { return h->scheme == OSBLI_RK3 ? 3 : 1; }
+
+}  // namespace
+
+extern "C" {
+
 int osbli_step(osbli_ctx *h, int n) {
   int u = check_usable(h);
   if (u) return u;
   if (n < 0) return fail(h, OSBLI_E_INVAL, "n must be >= 0");
-  static const double RK_A[3] = {0.0, -5.0 / 9.0, -153.0 / 128.0};
-  static const double RK_B[3] = {1.0 / 3.0, 15.0 / 16.0, 8.0 / 15.0};
-  const int nst = (h->scheme == OSBLI_RK3) ? 3 : 1;
+  if (h->loop) return fail(h, OSBLI_E_INVAL, "loopback slabs advance together: osbli_loopback_step");
   for (int it = 0; it < n; ++it) {
-    for (int s = 0; s < nst; ++s) {
-      KParams p = h->base;
-      if (h->scheme == OSBLI_RK3) {
-        p.A = RK_A[s];
-        p.B = RK_B[s];
-        p.read_w = (s > 0);
-        p.write_w = (s < 2);
-      } else {
-        p.A = 0.0;
-        p.B = 1.0;
-        p.read_w = 0;
-        p.write_w = 0;
-      }
-      double *qin = h->b.q[h->cur], *qout = h->b.q[h->cur ^ 1];
-      int r = exchange_ghosts(h, qin);
+    for (int s = 0; s < nstages(h); ++s) {
+      int r = run_stage(h, s);
       if (r) return r;
-      cudaEvent_t *ev = nullptr;
-      if (h->timing) {
-        if (h->ev_used + 3 > h->events.size()) {
-          for (int k = 0; k < 3; ++k) {
-            cudaEvent_t e;
-            CK(h, cudaEventCreate(&e));
-            h->events.push_back(e);
-          }
-        }
-        ev = &h->events[h->ev_used];
-        h->ev_used += 3;
-        CK(h, cudaEventRecord(ev[0], h->stream));
-      }
-      CK(h, osbli::launch_zpass(p, qin, h->b.rz, h->b.gz, 0, h->nz, h->stream, &h->launches));
-      if (ev) CK(h, cudaEventRecord(ev[1], h->stream));
-      CK(h, osbli::launch_xypass(p, qin, qout, h->b.w, h->b.rz, h->b.gz, nullptr, h->b.flag, 0,
-                                 h->nz, h->stream, &h->launches));
-      if (ev) CK(h, cudaEventRecord(ev[2], h->stream));
-      h->cur ^= 1;
     }
     ++h->step_count;
+  }
+  return OSBLI_OK;
+}
+
+int osbli_slab_bounds(int nz, int nranks, int rank, int *z0, int *nz_local) {
+  if (nz < 1 || nranks < 1 || rank < 0 || rank >= nranks || !z0 || !nz_local) return OSBLI_E_INVAL;
+  slab_partition(nz, nranks, rank, z0, nz_local);
+  return OSBLI_OK;
+}
+
+int osbli_ghost_plan(int rank, int nranks, int nz_local, int m, int *plan) {
+  if (nranks < 1 || rank < 0 || rank >= nranks || m < 1 || nz_local < m || !plan)
+    return OSBLI_E_INVAL;
+  ghost_plan(rank, nranks, nz_local, m, plan);
+  return OSBLI_OK;
+}
+
+int osbli_create_loopback(int nx, int ny, int nz, int order, double dx, double dt, double Re,
+                          double Pr, double Minf, double gamma, int scheme, int nslabs,
+                          osbli_ctx **out) {
+  if (!out || nslabs < 2) return OSBLI_E_INVAL;
+  std::string msg;
+  int v = validate(nx, ny, nz, order, dx, dt, Re, Pr, Minf, gamma, scheme, msg);
+  if (v != OSBLI_OK) { g_create_error = msg; return v; }
+  if (nz / nslabs < order / 2) { g_create_error = "every slab needs at least order/2 planes"; return OSBLI_E_INVAL; }
+  LoopGroup *g = new (std::nothrow) LoopGroup();
+  if (!g) return OSBLI_E_NOMEM;
+  for (int r = 0; r < nslabs; ++r) {
+    osbli_ctx *h = new (std::nothrow) osbli_ctx();
+    int rc = h ? OSBLI_OK : OSBLI_E_NOMEM;
+    if (h) {
+      slab_partition(nz, nslabs, r, &h->z0, &h->nz);
+      h->nx = nx; h->ny = ny; h->nz_global = nz;
+      h->order = order; h->scheme = scheme; h->rank = r; h->nranks = nslabs;
+      h->max_nz = nz / nslabs + (nz % nslabs ? 1 : 0);
+      h->dx = dx; h->dt = dt; h->Re = Re; h->Pr = Pr; h->Minf = Minf; h->gamma = gamma;
+      h->loop = g;
+      rc = create_common(h);
+      if (rc != OSBLI_OK) g_create_error = h->err;
+    }
+    if (rc != OSBLI_OK) {
+      if (h) { free_all(h); if (h->own_stream) cudaStreamDestroy(h->own_stream); delete h; }
+      for (auto *m : g->members) { free_all(m); if (m->own_stream) cudaStreamDestroy(m->own_stream); delete m; }
+      delete g;
+      return rc;
+    }
+    g->members.push_back(h);
+  }
+  // one stream for the whole group keeps the sibling copies ordered
+  for (int r = 0; r < nslabs; ++r) g->streams.push_back(g->members[r]->own_stream);
+  for (int r = 1; r < nslabs; ++r) g->members[r]->stream = g->members[0]->stream;
+  g->live = nslabs;
+  for (int r = 0; r < nslabs; ++r) out[r] = g->members[r];
+  return OSBLI_OK;
+}
+
+int osbli_loopback_step(osbli_ctx **hs, int nslabs, int n) {
+  if (!hs || nslabs < 2 || n < 0) return OSBLI_E_INVAL;
+  LoopGroup *g = hs[0] ? hs[0]->loop : nullptr;
+  if (!g || (int)g->members.size() != nslabs) return OSBLI_E_INVAL;
+  for (int r = 0; r < nslabs; ++r) {
+    if (hs[r] != g->members[r]) return OSBLI_E_INVAL;
+    int u = check_usable(hs[r]);
+    if (u) return u;
+  }
+  for (int it = 0; it < n; ++it) {
+    for (int s = 0; s < nstages(hs[0]); ++s) {
+      // every slab reads its neighbours' current planes, then all advance
+      for (int r = 0; r < nslabs; ++r) {
+        int rc = exchange_ghosts(hs[r], hs[r]->b.q[hs[r]->cur]);
+        if (rc) return rc;
+      }
+      for (int r = 0; r < nslabs; ++r) {
+        int rc = run_stage(hs[r], s, /*exchange=*/false);
+        if (rc) return rc;
+      }
+    }
+    for (int r = 0; r < nslabs; ++r) ++hs[r]->step_count;
   }
   return OSBLI_OK;
 }
@@ -445,34 +585,53 @@ int osbli_diagnostics(osbli_ctx *h, osbli_diag *out) {
   if (!out) return fail(h, OSBLI_E_INVAL, "null output pointer");
   int r = check_flag(h);
   if (r) return r;
-  double *qin = h->b.q[h->cur];
-  r = exchange_ghosts(h, qin);
-  if (r) return r;
-  CK(h, osbli::launch_diagnostics(h->base, qin, h->scratch, h->b.diag_part, h->stream,
-                                  &h->launches));
   std::vector<double> all;
   std::vector<int> counts;
-  if (h->nranks > 1) {
-    const int base = h->nz_global / h->nranks, extra = h->nz_global % h->nranks;
-    CK(h, cudaMemsetAsync(h->nccl_part, 0, (size_t)3 * h->nranks * h->max_nz * sizeof(double),
-                          h->stream));
-    // gather padded per-plane partials; every rank then sums in global plane order
-    NK(h, ncclAllGather(h->b.diag_part, h->nccl_part, (size_t)3 * h->max_nz, ncclDouble, h->comm,
-                        h->stream));
-    all.resize((size_t)3 * h->nranks * h->max_nz);
-    CK(h, cudaMemcpyAsync(all.data(), h->nccl_part, all.size() * sizeof(double),
-                          cudaMemcpyDeviceToHost, h->stream));
-    for (int rr = 0; rr < h->nranks; ++rr) counts.push_back(base + (rr < extra ? 1 : 0));
+  int stride = h->nz;
+  if (h->loop) {
+    // loopback slabs: every sibling computes its per-plane partials; gathered in rank order
+    stride = h->max_nz;
+    all.assign((size_t)3 * h->nranks * stride, 0.0);
+    for (osbli_ctx *m : h->loop->members) {
+      r = exchange_ghosts(m, m->b.q[m->cur]);
+      if (r) return r;
+      CK(h, osbli::launch_diagnostics(m->base, m->b.q[m->cur], m->scratch, m->b.diag_part,
+                                      m->stream, &m->launches));
+      CK(h, cudaMemcpyAsync(all.data() + (size_t)3 * m->rank * stride, m->b.diag_part,
+                            (size_t)3 * m->nz * sizeof(double), cudaMemcpyDeviceToHost, m->stream));
+      counts.push_back(m->nz);
+    }
   } else {
-    all.resize((size_t)3 * h->nz);
-    CK(h, cudaMemcpyAsync(all.data(), h->b.diag_part, all.size() * sizeof(double),
-                          cudaMemcpyDeviceToHost, h->stream));
-    counts.push_back(h->nz);
+    double *qin = h->b.q[h->cur];
+    r = exchange_ghosts(h, qin);
+    if (r) return r;
+    CK(h, osbli::launch_diagnostics(h->base, qin, h->scratch, h->b.diag_part, h->stream,
+                                    &h->launches));
+    if (h->nranks > 1) {
+      stride = h->max_nz;
+      CK(h, cudaMemsetAsync(h->nccl_part, 0, (size_t)3 * h->nranks * h->max_nz * sizeof(double),
+                            h->stream));
+      // gather padded per-plane partials; every rank then sums in global plane order
+      NK(h, ncclAllGather(h->b.diag_part, h->nccl_part, (size_t)3 * h->max_nz, ncclDouble,
+                          h->comm, h->stream));
+      all.resize((size_t)3 * h->nranks * h->max_nz);
+      CK(h, cudaMemcpyAsync(all.data(), h->nccl_part, all.size() * sizeof(double),
+                            cudaMemcpyDeviceToHost, h->stream));
+      for (int rr = 0; rr < h->nranks; ++rr) {
+        int z0 = 0, nzl = 0;
+        slab_partition(h->nz_global, h->nranks, rr, &z0, &nzl);
+        counts.push_back(nzl);
+      }
+    } else {
+      all.resize((size_t)3 * h->nz);
+      CK(h, cudaMemcpyAsync(all.data(), h->b.diag_part, all.size() * sizeof(double),
+                            cudaMemcpyDeviceToHost, h->stream));
+      counts.push_back(h->nz);
+    }
   }
   CK(h, cudaStreamSynchronize(h->stream));
   // Neumaier sums over planes in global z order
   double s[3] = {0, 0, 0}, c[3] = {0, 0, 0};
-  const int stride = (h->nranks > 1) ? h->max_nz : h->nz;
   for (int rr = 0; rr < (int)counts.size(); ++rr)
     for (int z = 0; z < counts[rr]; ++z)
       for (int k = 0; k < 3; ++k) {
@@ -538,7 +697,18 @@ void osbli_destroy(osbli_ctx *h) {
   if (h->comm) ncclCommDestroy(h->comm);
   for (auto e : h->events) cudaEventDestroy(e);
   free_all(h);
-  if (h->own_stream) cudaStreamDestroy(h->own_stream);
+  LoopGroup *g = h->loop;
+  if (g) {
+    // the group stream belongs to member 0: destroy streams with the last member
+    for (auto &m : g->members)
+      if (m == h) m = nullptr;
+    if (--g->live == 0) {
+      for (cudaStream_t st : g_loop_streams(g)) cudaStreamDestroy(st);
+      delete g;
+    }
+  } else if (h->own_stream) {
+    cudaStreamDestroy(h->own_stream);
+  }
   delete h;
 }
 

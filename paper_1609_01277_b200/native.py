@@ -71,6 +71,13 @@ def load():
     L.osbli_kernel_timing.argtypes = [H, ctypes.POINTER(c_double), ctypes.POINTER(c_double),
                                       ctypes.POINTER(ctypes.c_longlong),
                                       ctypes.POINTER(ctypes.c_longlong)]
+    ip = ctypes.POINTER(c_int)
+    L.osbli_slab_bounds.argtypes = [c_int, c_int, c_int, ip, ip]
+    L.osbli_ghost_plan.argtypes = [c_int, c_int, c_int, c_int, ip]
+    L.osbli_create_loopback.argtypes = [c_int, c_int, c_int, c_int, c_double, c_double, c_double,
+                                        c_double, c_double, c_double, c_int, c_int,
+                                        ctypes.POINTER(H)]
+    L.osbli_loopback_step.argtypes = [ctypes.POINTER(H), c_int, c_int]
     L.osbli_kernel_launches.argtypes = [H]
     L.osbli_kernel_launches.restype = ctypes.c_longlong
     L.osbli_last_error.argtypes = [H]
@@ -92,6 +99,24 @@ def nccl_unique_id() -> bytes:
     if rc != 0:
         raise OsbliError(rc, load().osbli_last_error(None).decode())
     return buf.raw
+
+
+def slab_bounds(nz: int, nranks: int, rank: int):
+    """(z0, nz_local) from the library's partition rule (host-only, no GPU)."""
+    z0, nzl = ctypes.c_int(), ctypes.c_int()
+    rc = load().osbli_slab_bounds(nz, nranks, rank, ctypes.byref(z0), ctypes.byref(nzl))
+    if rc != 0:
+        raise OsbliError(rc, "invalid slab arguments")
+    return z0.value, nzl.value
+
+
+def ghost_plan(rank: int, nranks: int, nz_local: int, m: int):
+    """The library's ghost-exchange plan: [(send_peer, send_plane, recv_peer, recv_plane)] x 2."""
+    plan = (ctypes.c_int * 8)()
+    rc = load().osbli_ghost_plan(rank, nranks, nz_local, m, plan)
+    if rc != 0:
+        raise OsbliError(rc, "invalid ghost-plan arguments")
+    return [tuple(plan[4 * t:4 * t + 4]) for t in range(2)]
 
 
 def _ptr(a):
@@ -193,6 +218,17 @@ class Solver:
     def kernel_launches(self) -> int:
         return int(self._L.osbli_kernel_launches(self._h))
 
+    @classmethod
+    def _wrap(cls, L, h, nx, ny, nz_global, order):
+        self = cls.__new__(cls)
+        self._L, self._h = L, h
+        self.nx, self.ny, self.nz_global, self.order = nx, ny, nz_global, order
+        z0, nzl = ctypes.c_int(), ctypes.c_int()
+        L.osbli_local_box(self._h, ctypes.byref(z0), ctypes.byref(nzl))
+        self.z0, self.nz = z0.value, nzl.value
+        self.shape = (5, self.nz, ny, nx)
+        return self
+
     def close(self):
         if self._h:
             self._L.osbli_destroy(self._h)
@@ -209,6 +245,39 @@ class Solver:
 
     def __exit__(self, *a):
         self.close()
+
+
+class LoopbackGroup:
+    """nslabs z-slab handles on one GPU exchanging ghost planes by device copies
+    (osbli_create_loopback): the distributed kernel path without NCCL."""
+
+    def __init__(self, nx, ny, nz, order, dx, dt, nslabs, Re=1600.0, Pr=0.71, Minf=0.1,
+                 gamma=1.4, scheme=OSBLI_RK3):
+        L = load()
+        arr = (ctypes.c_void_p * nslabs)()
+        rc = L.osbli_create_loopback(nx, ny, nz, order, dx, dt, Re, Pr, Minf, gamma, scheme,
+                                     nslabs, arr)
+        if rc != 0:
+            raise OsbliError(rc, L.osbli_last_error(None).decode())
+        self._L, self._arr = L, arr
+        self.slabs = [Solver._wrap(L, ctypes.c_void_p(arr[i]), nx, ny, nz, order)
+                      for i in range(nslabs)]
+
+    def set_state(self, q):
+        for s in self.slabs:
+            s.set_state(np.ascontiguousarray(q[:, s.z0:s.z0 + s.nz]))
+
+    def get_state(self):
+        return np.concatenate([s.get_state() for s in self.slabs], axis=1)
+
+    def step(self, n=1):
+        rc = self._L.osbli_loopback_step(self._arr, len(self.slabs), int(n))
+        if rc != 0:
+            raise OsbliError(rc, self._L.osbli_last_error(self.slabs[0]._h).decode())
+
+    def close(self):
+        for s in self.slabs:
+            s.close()
 
 
 def inviscid() -> float:
