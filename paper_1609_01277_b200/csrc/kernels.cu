@@ -41,173 +41,16 @@ __device__ __forceinline__ int zread(const KParams &p, int z) {
   return max(-p.G, min(z, p.nz - 1 + p.G));
 }
 
-// ------------------------------------------------------------------ z-pass
-constexpr int ZP_TX = 32;
-constexpr int ZP_TZ = 32;
-constexpr int ZP_RZ = 4;
-constexpr int ZP_THREADS = 32 * (ZP_TZ / ZP_RZ);  // 256
-constexpr int ZP_NF = 13;
-// staged operand slots
-enum { ZS_RHO = 0, ZS_M0, ZS_M1, ZS_M2, ZS_E, ZS_U0, ZS_U1, ZS_U2, ZS_T, ZS_F0, ZS_F1, ZS_F2, ZS_G };
-
-template <int M>
-constexpr int zp_smem_bytes() {
-  return ZP_NF * (ZP_TZ + 2 * M) * 32 * (int)sizeof(double);
+// 8-byte asynchronous global -> shared copy (LDGSTS), completed by cp_async_wait_all
+__device__ __forceinline__ void cp_async8(double *smem, const double *gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
 
-template <int M>
-__device__ __forceinline__ void zwindow(const double *S, int f, int pbase, int lane,
-                                        double (&v)[ZP_RZ + 2 * M]) {
-  constexpr int NP = ZP_TZ + 2 * M;
-#pragma unroll
-  for (int t = 0; t < ZP_RZ + 2 * M; ++t) v[t] = S[(f * NP + pbase + t) * 32 + lane];
-}
-
-template <int M>
-__device__ __forceinline__ double d1w(const KParams &p, const double (&v)[ZP_RZ + 2 * M], int j) {
-  double s = 0.0;
-#pragma unroll
-  for (int k = 1; k <= M; ++k) s = fma(p.a[k - 1], v[j + M + k] - v[j + M - k], s);
-  return s;
-}
-
-template <int M>
-__device__ __forceinline__ double d2w(const KParams &p, const double (&v)[ZP_RZ + 2 * M], int j) {
-  const double c = v[j + M];
-  double s = 0.0;
-#pragma unroll
-  for (int k = 1; k <= M; ++k) s = fma(p.b[k], (v[j + M + k] - c) + (v[j + M - k] - c), s);
-  return s;
-}
-
-template <int M>
-__global__ void __launch_bounds__(ZP_THREADS, 1)
-    zpass_kernel(const KParams p, const double *__restrict__ q, double *__restrict__ rz,
-                 double *__restrict__ gz, int z_begin, int z_end) {
-  extern __shared__ double S[];
-  constexpr int NP = ZP_TZ + 2 * M;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int x0 = blockIdx.x * ZP_TX, y = blockIdx.y;
-  const int z0 = z_begin + blockIdx.z * ZP_TZ;
-  const size_t FS = (size_t)p.nx * p.ny;
-
-  // ---- stage the z-stencil operands of NP planes x 32 columns (formulas);
-  //      all global loads of a thread are issued before the first shared store
-  constexpr int NIT = (NP * 32 + ZP_THREADS - 1) / ZP_THREADS;
-  double raw[NIT][5];
-#pragma unroll
-  for (int it = 0; it < NIT; ++it) {
-    const int idx = threadIdx.x + it * ZP_THREADS;
-    if (idx < NP * 32) {
-      const int pl = idx >> 5, c = idx & 31;
-      int x = x0 + c;
-      if (x >= p.nx) x = wrapi(x, p.nx);
-      const int z = zread(p, z0 - M + pl);
-      const double *qp = q + qplane(p, z) + (size_t)y * p.nx + x;
-#pragma unroll
-      for (int f = 0; f < 5; ++f) raw[it][f] = __ldg(qp + f * FS);
-    }
-  }
-#pragma unroll
-  for (int it = 0; it < NIT; ++it) {
-    const int idx = threadIdx.x + it * ZP_THREADS;
-    if (idx < NP * 32) {
-      const int pl = idx >> 5, c = idx & 31;
-      const double rho = raw[it][0], m0 = raw[it][1], m1 = raw[it][2], m2 = raw[it][3],
-                   e = raw[it][4];
-      const double r = 1.0 / rho;
-      const double u0 = m0 * r, u1 = m1 * r, u2 = m2 * r;
-      const double pr = p.gm1 * (e - 0.5 * (m0 * u0 + m1 * u1 + m2 * u2));
-      const double T = p.gM2 * pr * r;
-      double *s = S + pl * 32 + c;
-      s[ZS_RHO * NP * 32] = rho;
-      s[ZS_M0 * NP * 32] = m0;
-      s[ZS_M1 * NP * 32] = m1;
-      s[ZS_M2 * NP * 32] = m2;
-      s[ZS_E * NP * 32] = e;
-      s[ZS_U0 * NP * 32] = u0;
-      s[ZS_U1 * NP * 32] = u1;
-      s[ZS_U2 * NP * 32] = u2;
-      s[ZS_T * NP * 32] = T;
-      // momentum flux F_i2 = 1/2 m_i u_2 + delta_i2 p  (skew half + pressure)
-      s[ZS_F0 * NP * 32] = 0.5 * m0 * u2;
-      s[ZS_F1 * NP * 32] = 0.5 * m1 * u2;
-      s[ZS_F2 * NP * 32] = 0.5 * m2 * u2 + pr;
-      // energy flux G_2 = (1/2 e + p) u_2  (skew half + pressure work)
-      s[ZS_G * NP * 32] = (0.5 * e + pr) * u2;
-    }
-  }
-  __syncthreads();
-
-  const int pbase = warp * ZP_RZ;
-  double v[ZP_RZ + 2 * M];
-  double g[3][ZP_RZ], R[5][ZP_RZ], u2c[ZP_RZ];
-
-  // velocity: g_i2 = D_z u_i, viscous z-Laplacian parts of V_i and u_i V_i
-  zwindow<M>(S, ZS_U2, pbase, lane, v);
-  double d2u2[ZP_RZ];
-#pragma unroll
-  for (int j = 0; j < ZP_RZ; ++j) {
-    g[2][j] = d1w<M>(p, v, j);
-    d2u2[j] = d2w<M>(p, v, j);
-    u2c[j] = v[j + M];
-    const double V2 = p.nu * (d2u2[j] + (1.0 / 3.0) * d2u2[j]);
-    R[3][j] = V2;
-    R[4][j] = u2c[j] * V2;
-  }
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    zwindow<M>(S, ZS_U0 + i, pbase, lane, v);
-#pragma unroll
-    for (int j = 0; j < ZP_RZ; ++j) {
-      g[i][j] = d1w<M>(p, v, j);
-      const double Vi = p.nu * d2w<M>(p, v, j);
-      R[1 + i][j] = Vi;
-      R[4][j] = fma(v[j + M], Vi, R[4][j]);
-    }
-  }
-  // heat flux: kappa D_zz T
-  zwindow<M>(S, ZS_T, pbase, lane, v);
-#pragma unroll
-  for (int j = 0; j < ZP_RZ; ++j) R[4][j] = fma(p.kappa, d2w<M>(p, v, j), R[4][j]);
-  // skew advective + dilatation halves: -1/2 (u_2 D_z s + s g_22) for s = rho, m_i, e
-#pragma unroll
-  for (int f = 0; f < 5; ++f) {
-    zwindow<M>(S, ZS_RHO + f, pbase, lane, v);
-#pragma unroll
-    for (int j = 0; j < ZP_RZ; ++j) {
-      const double ds = d1w<M>(p, v, j);
-      const double t = fma(u2c[j], ds, v[j + M] * g[2][j]);
-      if (f == 0) R[0][j] = -0.5 * t;
-      else R[f][j] = fma(-0.5, t, R[f][j]);
-      if (f == 3) R[0][j] = fma(-0.5, ds, R[0][j]);  // mass flux D_z(rho u_2) = D_z m_2
-    }
-  }
-  // conservative flux halves: -D_z F_i2, -D_z G_2
-#pragma unroll
-  for (int f = 0; f < 4; ++f) {
-    zwindow<M>(S, ZS_F0 + f, pbase, lane, v);
-#pragma unroll
-    for (int j = 0; j < ZP_RZ; ++j) R[1 + f][j] -= d1w<M>(p, v, j);
-  }
-
-  const int x = x0 + lane;
-  if (x < p.nx) {
-#pragma unroll
-    for (int j = 0; j < ZP_RZ; ++j) {
-      const int z = z0 + pbase + j;
-      if (z < z_end) {
-        const size_t o = (size_t)z * 5 * FS + (size_t)y * p.nx + x;
-#pragma unroll
-        for (int f = 0; f < 5; ++f) rz[o + f * FS] = R[f][j];
-        const size_t og = (size_t)z * 3 * FS + (size_t)y * p.nx + x;
-#pragma unroll
-        for (int i = 0; i < 3; ++i) gz[og + i * FS] = g[i][j];
-      }
-    }
-  }
-}
-
+#include "zpass.cuh"
 #include "xypass.cuh"
 
 // ------------------------------------------------------------------ diagnostics
@@ -331,8 +174,15 @@ cudaError_t zpass_launch(const KParams &p, const double *q, double *rz, double *
     if (e != cudaSuccess) return e;
     init = true;
   }
-  dim3 grid((p.nx + ZP_TX - 1) / ZP_TX, p.ny, (ze - zb + ZP_TZ - 1) / ZP_TZ);
-  zpass_kernel<M><<<grid, ZP_THREADS, smem, s>>>(p, q, rz, gz, zb, ze);
+  const int gx = (p.nx + ZP_TX - 1) / ZP_TX, gy = p.ny;
+  const int chunks = (ze - zb + ZP_TZ - 1) / ZP_TZ;
+  // split the z-range into segments only when the pencils alone do not fill ~2 waves
+  int nseg = (2 * 148 + gx * gy - 1) / (gx * gy);
+  nseg = nseg < 1 ? 1 : (nseg > chunks ? chunks : nseg);
+  const int seg_len = ((chunks + nseg - 1) / nseg) * ZP_TZ;
+  nseg = (ze - zb + seg_len - 1) / seg_len;
+  dim3 grid(gx, gy, nseg);
+  zpass_kernel<M><<<grid, ZP_THREADS, smem, s>>>(p, q, rz, gz, zb, ze, seg_len);
   return cudaGetLastError();
 }
 

@@ -42,15 +42,6 @@ struct XYGeom {
   static constexpr int BYTES = TOTAL * (int)sizeof(double);
 };
 
-// 8-byte asynchronous global -> shared copy (LDGSTS), completed by cp_async_wait_all
-__device__ __forceinline__ void cp_async8(double *smem, const double *gmem) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
-}
-
 template <int M>
 constexpr int xy_smem_bytes() {
   return XYGeom<M>::BYTES;

@@ -1,0 +1,232 @@
+// z-pass (included by kernels.cu inside namespace osbli::{anon}).
+//
+// Every term of the residual that differentiates along z (D_z, D_zz; the z
+// halves of the skew-symmetric terms P:271-274, the z fluxes, the z parts of
+// the viscous Laplacians P:274 and of the heat flux), written as a partial
+// residual Rz[5], plus g_i2 = D_z u_i for the xy-pass.
+//
+// A CTA owns a pencil of 32 x-columns x one y-row and marches through its
+// z-range in chunks of TZ = 32 planes.  Shared memory holds a ring of
+// NR = TZ + 2m planes of the 13 z-stencil operands (formulas computed once per
+// plane): consecutive chunks share their 2m overlap planes, so every
+// plane is loaded from HBM once.  While chunk k is computed, the raw state of
+// the TZ planes chunk k+1 adds is already in flight into a staging buffer
+// (cp.async), so the HBM latency hides behind the FP64 work.  Each thread
+// produces RZ = 4 consecutive z outputs of its column from register windows.
+constexpr int ZP_TX = 32;
+constexpr int ZP_TZ = 32;
+constexpr int ZP_RZ = 4;
+constexpr int ZP_THREADS = 32 * (ZP_TZ / ZP_RZ);  // 256
+constexpr int ZP_NF = 13;
+// staged operand slots
+enum { ZS_RHO = 0, ZS_M0, ZS_M1, ZS_M2, ZS_E, ZS_U0, ZS_U1, ZS_U2, ZS_T, ZS_F0, ZS_F1, ZS_F2, ZS_G };
+
+template <int M>
+struct ZGeom {
+  static constexpr int NR = ZP_TZ + 2 * M;      // ring slots (planes)
+  static constexpr int RING = ZP_NF * NR * 32;  // doubles
+  static constexpr int RAW = 5 * ZP_TZ * 32;    // raw planes of the next chunk
+  static constexpr int BYTES = (RING + RAW) * (int)sizeof(double);
+};
+
+template <int M>
+constexpr int zp_smem_bytes() {
+  return ZGeom<M>::BYTES;
+}
+
+// formulas of one staged point into ring slot `slot`, column c
+template <int M>
+__device__ __forceinline__ void zstore(const KParams &p, double *S, int slot, int c, double rho,
+                                       double m0, double m1, double m2, double e) {
+  constexpr int NR = ZGeom<M>::NR;
+  const double r = 1.0 / rho;
+  const double u0 = m0 * r, u1 = m1 * r, u2 = m2 * r;
+  const double pr = p.gm1 * (e - 0.5 * (m0 * u0 + m1 * u1 + m2 * u2));
+  const double T = p.gM2 * pr * r;
+  double *s = S + slot * 32 + c;
+  s[ZS_RHO * NR * 32] = rho;
+  s[ZS_M0 * NR * 32] = m0;
+  s[ZS_M1 * NR * 32] = m1;
+  s[ZS_M2 * NR * 32] = m2;
+  s[ZS_E * NR * 32] = e;
+  s[ZS_U0 * NR * 32] = u0;
+  s[ZS_U1 * NR * 32] = u1;
+  s[ZS_U2 * NR * 32] = u2;
+  s[ZS_T * NR * 32] = T;
+  // momentum flux F_i2 = 1/2 m_i u_2 + delta_i2 p  (skew half + pressure)
+  s[ZS_F0 * NR * 32] = 0.5 * m0 * u2;
+  s[ZS_F1 * NR * 32] = 0.5 * m1 * u2;
+  s[ZS_F2 * NR * 32] = 0.5 * m2 * u2 + pr;
+  // energy flux G_2 = (1/2 e + p) u_2  (skew half + pressure work)
+  s[ZS_G * NR * 32] = (0.5 * e + pr) * u2;
+}
+
+// register window of ring field f starting at ring slot slot0 (wraps modulo NR)
+template <int M>
+__device__ __forceinline__ void zwindow(const double *S, int f, int slot0, int lane,
+                                        double (&v)[ZP_RZ + 2 * M]) {
+  constexpr int NR = ZGeom<M>::NR;
+#pragma unroll
+  for (int t = 0; t < ZP_RZ + 2 * M; ++t) {
+    int sl = slot0 + t;
+    if (sl >= NR) sl -= NR;
+    v[t] = S[(f * NR + sl) * 32 + lane];
+  }
+}
+
+template <int M>
+__device__ __forceinline__ double d1w(const KParams &p, const double (&v)[ZP_RZ + 2 * M], int j) {
+  double s = 0.0;
+#pragma unroll
+  for (int k = 1; k <= M; ++k) s = fma(p.a[k - 1], v[j + M + k] - v[j + M - k], s);
+  return s;
+}
+
+// exactly zero on a constant window (D-22)
+template <int M>
+__device__ __forceinline__ double d2w(const KParams &p, const double (&v)[ZP_RZ + 2 * M], int j) {
+  const double c = v[j + M];
+  double s = 0.0;
+#pragma unroll
+  for (int k = 1; k <= M; ++k) s = fma(p.b[k], fma(-2.0, c, v[j + M + k] + v[j + M - k]), s);
+  return s;
+}
+
+template <int M>
+__global__ void __launch_bounds__(ZP_THREADS, 1)
+    zpass_kernel(const KParams p, const double *__restrict__ q, double *__restrict__ rz,
+                 double *__restrict__ gz, int z_begin, int z_end, int seg_len) {
+  using Zg = ZGeom<M>;
+  constexpr int NR = Zg::NR;
+  extern __shared__ double S[];
+  double *RB = S + Zg::RING;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int x0 = blockIdx.x * ZP_TX, y = blockIdx.y;
+  const int zs = z_begin + blockIdx.z * seg_len;
+  const int ze = min(z_end, zs + seg_len);
+  if (zs >= ze) return;
+  const int nchunks = (ze - zs + ZP_TZ - 1) / ZP_TZ;
+  const size_t FS = (size_t)p.nx * p.ny;
+  // column this thread loads for staging slot c = tid & 31 (ragged tiles load any valid column)
+  int xc = x0 + lane;
+  if (xc >= p.nx) xc = wrapi(xc, p.nx);
+  const size_t rowoff = (size_t)y * p.nx + xc;
+
+  // ---- prologue: ring planes zl = 0..NR-1 (z = zs - M + zl), all loads in flight first
+  {
+    constexpr int NIT = (NR * 32 + ZP_THREADS - 1) / ZP_THREADS;
+    double raw[NIT][5];
+#pragma unroll
+    for (int it = 0; it < NIT; ++it) {
+      const int idx = tid + it * ZP_THREADS;
+      if (idx < NR * 32) {
+        const int pl = idx >> 5;
+        const double *qp = q + qplane(p, zread(p, zs - M + pl)) + rowoff;
+#pragma unroll
+        for (int f = 0; f < 5; ++f) raw[it][f] = __ldg(qp + f * FS);
+      }
+    }
+#pragma unroll
+    for (int it = 0; it < NIT; ++it) {
+      const int idx = tid + it * ZP_THREADS;
+      if (idx < NR * 32)
+        zstore<M>(p, S, idx >> 5, lane, raw[it][0], raw[it][1], raw[it][2], raw[it][3],
+                  raw[it][4]);
+    }
+  }
+  // raw planes of chunk kk: z = zs + kk*TZ + M + j, j = 0..TZ-1  ->  RB[f][j][c]
+  auto issue_raw = [&](int kk) {
+    for (int idx = tid; idx < ZP_TZ * 32; idx += ZP_THREADS) {
+      const int j = idx >> 5;
+      const double *qp = q + qplane(p, zread(p, zs + kk * ZP_TZ + M + j)) + rowoff;
+#pragma unroll
+      for (int f = 0; f < 5; ++f) cp_async8(RB + (f * ZP_TZ + j) * 32 + lane, qp + f * FS);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  if (nchunks > 1) issue_raw(1);
+  __syncthreads();
+
+  for (int k = 0; k < nchunks; ++k) {
+    // ---- compute chunk k: outputs z = zs + k*TZ + warp*RZ + j
+    const int zl0 = k * ZP_TZ + warp * ZP_RZ;  // local index of the window's first plane
+    const int slot0 = zl0 % NR;
+    double v[ZP_RZ + 2 * M];
+    double g[3][ZP_RZ], R[5][ZP_RZ], u2c[ZP_RZ];
+    // velocity: g_i2 = D_z u_i, z-Laplacian parts of V_i and u_i V_i
+    zwindow<M>(S, ZS_U2, slot0, lane, v);
+#pragma unroll
+    for (int j = 0; j < ZP_RZ; ++j) {
+      g[2][j] = d1w<M>(p, v, j);
+      const double d2u2 = d2w<M>(p, v, j);
+      u2c[j] = v[j + M];
+      const double V2 = p.nu * (d2u2 + (1.0 / 3.0) * d2u2);
+      R[3][j] = V2;
+      R[4][j] = u2c[j] * V2;
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      zwindow<M>(S, ZS_U0 + i, slot0, lane, v);
+#pragma unroll
+      for (int j = 0; j < ZP_RZ; ++j) {
+        g[i][j] = d1w<M>(p, v, j);
+        const double Vi = p.nu * d2w<M>(p, v, j);
+        R[1 + i][j] = Vi;
+        R[4][j] = fma(v[j + M], Vi, R[4][j]);
+      }
+    }
+    // heat flux: kappa D_zz T
+    zwindow<M>(S, ZS_T, slot0, lane, v);
+#pragma unroll
+    for (int j = 0; j < ZP_RZ; ++j) R[4][j] = fma(p.kappa, d2w<M>(p, v, j), R[4][j]);
+    // skew advective + dilatation halves: -1/2 (u_2 D_z s + s g_22), s = rho, m_i, e
+#pragma unroll
+    for (int f = 0; f < 5; ++f) {
+      zwindow<M>(S, ZS_RHO + f, slot0, lane, v);
+#pragma unroll
+      for (int j = 0; j < ZP_RZ; ++j) {
+        const double ds = d1w<M>(p, v, j);
+        const double t = fma(u2c[j], ds, v[j + M] * g[2][j]);
+        if (f == 0) R[0][j] = -0.5 * t;
+        else R[f][j] = fma(-0.5, t, R[f][j]);
+        if (f == 3) R[0][j] = fma(-0.5, ds, R[0][j]);  // mass flux D_z(rho u_2) = D_z m_2
+      }
+    }
+    // conservative flux halves: -D_z F_i2, -D_z G_2
+#pragma unroll
+    for (int f = 0; f < 4; ++f) {
+      zwindow<M>(S, ZS_F0 + f, slot0, lane, v);
+#pragma unroll
+      for (int j = 0; j < ZP_RZ; ++j) R[1 + f][j] -= d1w<M>(p, v, j);
+    }
+    const int x = x0 + lane;
+    if (x < p.nx) {
+#pragma unroll
+      for (int j = 0; j < ZP_RZ; ++j) {
+        const int z = zs + zl0 + j;
+        if (z < ze) {
+          const size_t o = (size_t)z * 5 * FS + (size_t)y * p.nx + x;
+#pragma unroll
+          for (int f = 0; f < 5; ++f) rz[o + f * FS] = R[f][j];
+          const size_t og = (size_t)z * 3 * FS + (size_t)y * p.nx + x;
+#pragma unroll
+          for (int i = 0; i < 3; ++i) gz[og + i * FS] = g[i][j];
+        }
+      }
+    }
+    if (k + 1 < nchunks) {
+      // ---- advance the ring: planes of chunk k+1 replace the first TZ planes of chunk k
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      __syncthreads();  // staged raw planes visible; every warp is done with chunk k
+      for (int idx = tid; idx < ZP_TZ * 32; idx += ZP_THREADS) {
+        const int j = idx >> 5;
+        const int slot = ((k + 1) * ZP_TZ + 2 * M + j) % NR;
+        zstore<M>(p, S, slot, lane, RB[(0 * ZP_TZ + j) * 32 + lane],
+                  RB[(1 * ZP_TZ + j) * 32 + lane], RB[(2 * ZP_TZ + j) * 32 + lane],
+                  RB[(3 * ZP_TZ + j) * 32 + lane], RB[(4 * ZP_TZ + j) * 32 + lane]);
+      }
+      __syncthreads();  // ring updated, staging buffer free
+      if (k + 2 < nchunks) issue_raw(k + 2);
+    }
+  }
+}
