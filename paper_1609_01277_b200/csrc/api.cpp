@@ -152,7 +152,6 @@ void free_all(osbli_ctx *h) {
   cudaFree(h->b.q[0]);
   cudaFree(h->b.q[1]);
   cudaFree(h->b.w);
-  cudaFree(h->b.rz);
   cudaFree(h->b.gz);
   cudaFree(h->b.flag);
   cudaFree(h->b.diag_part);
@@ -175,7 +174,6 @@ int create_common(osbli_ctx *h) {
   cudaError_t e = cudaSuccess;
   if ((e = alloc(&h->b.q[0], qn)) != cudaSuccess || (e = alloc(&h->b.q[1], qn)) != cudaSuccess ||
       (e = alloc(&h->b.w, (size_t)h->nz * 5 * FS)) != cudaSuccess ||
-      (e = alloc(&h->b.rz, (size_t)h->nz * 5 * FS)) != cudaSuccess ||
       (e = alloc(&h->b.gz, (size_t)h->nz * 3 * FS)) != cudaSuccess ||
       (e = alloc(&h->scratch, (size_t)(h->nz + 2 * G) * 3 * FS)) != cudaSuccess ||
       (e = alloc(&h->b.diag_part, (size_t)3 * h->nz)) != cudaSuccess ||
@@ -395,10 +393,11 @@ int osbli_set_state(osbli_ctx *h, const double *q, int on_device) {
   if (u) return u;
   if (!q) return fail(h, OSBLI_E_INVAL, "null state pointer");
   const size_t n = (size_t)5 * h->nz * h->nx * h->ny;
-  // stage in ABI layout through the z-pass scratch (Rz), then transpose
-  CK(h, cudaMemcpyAsync(h->b.rz, q, n * sizeof(double),
+  // stage in ABI layout through the idle ping-pong buffer, then transpose
+  double *stage = h->b.q[h->cur ^ 1];
+  CK(h, cudaMemcpyAsync(stage, q, n * sizeof(double),
                         on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, h->stream));
-  CK(h, osbli::launch_abi_to_internal(h->base, h->b.rz, h->b.q[h->cur], h->stream, &h->launches));
+  CK(h, osbli::launch_abi_to_internal(h->base, stage, h->b.q[h->cur], h->stream, &h->launches));
   CK(h, cudaMemsetAsync(h->b.flag, 0, sizeof(unsigned int), h->stream));
   CK(h, cudaStreamSynchronize(h->stream));
   h->step_count = 0;
@@ -408,8 +407,9 @@ int osbli_set_state(osbli_ctx *h, const double *q, int on_device) {
 int osbli_get_state(osbli_ctx *h, double *q, int on_device) {
   if (!h || !q) return OSBLI_E_INVAL;
   const size_t n = (size_t)5 * h->nz * h->nx * h->ny;
-  CK(h, osbli::launch_internal_to_abi(h->base, h->b.q[h->cur], h->b.rz, 5, 1, h->stream, &h->launches));
-  CK(h, cudaMemcpyAsync(q, h->b.rz, n * sizeof(double),
+  double *stage = h->b.q[h->cur ^ 1];  // idle ping-pong buffer as ABI-layout staging
+  CK(h, osbli::launch_internal_to_abi(h->base, h->b.q[h->cur], stage, 5, 1, h->stream, &h->launches));
+  CK(h, cudaMemcpyAsync(q, stage, n * sizeof(double),
                         on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, h->stream));
   CK(h, cudaStreamSynchronize(h->stream));
   return OSBLI_OK;
@@ -453,9 +453,9 @@ int run_stage(osbli_ctx *h, int s, bool exchange = true) {
     h->ev_used += 3;
     CK(h, cudaEventRecord(ev[0], h->stream));
   }
-  CK(h, osbli::launch_zpass(p, qin, h->b.rz, h->b.gz, 0, h->nz, h->stream, &h->launches));
+  CK(h, osbli::launch_zpass(p, qin, h->b.w, h->b.gz, 0, h->nz, h->stream, &h->launches));
   if (ev) CK(h, cudaEventRecord(ev[1], h->stream));
-  CK(h, osbli::launch_xypass(p, qin, qout, h->b.w, h->b.rz, h->b.gz, nullptr, h->b.flag, 0, h->nz,
+  CK(h, osbli::launch_xypass(p, qin, qout, h->b.w, h->b.gz, nullptr, h->b.flag, 0, h->nz,
                              h->stream, &h->launches));
   if (ev) CK(h, cudaEventRecord(ev[2], h->stream));
   h->cur ^= 1;
@@ -569,11 +569,19 @@ int osbli_residual(osbli_ctx *h, double *R, int on_device) {
   double *qin = h->b.q[h->cur];
   int r = exchange_ghosts(h, qin);
   if (r) return r;
-  // R lands in W ([nz][5] plane-major), then is transposed into Rz (ABI layout)
-  CK(h, osbli::launch_stage(h->base, qin, nullptr, h->b.w, h->b.rz, h->b.gz, h->b.w, h->b.flag,
-                            h->stream, &h->launches));
-  CK(h, osbli::launch_internal_to_abi(h->base, h->b.w, h->b.rz, 5, 0, h->stream, &h->launches));
-  CK(h, cudaMemcpyAsync(R, h->b.rz, n * sizeof(double),
+  // R lands in W ([nz][5] plane-major: A = 0, dt = 1 so that W' = Rz and R = W' + R_xy),
+  // then is transposed into the idle ping-pong buffer (ABI layout)
+  KParams p = h->base;
+  p.A = 0.0;
+  p.B = 0.0;
+  p.dt = 1.0;
+  p.read_w = 0;
+  p.write_w = 0;
+  double *stage = h->b.q[h->cur ^ 1];
+  CK(h, osbli::launch_stage(p, qin, nullptr, h->b.w, h->b.gz, h->b.w, h->b.flag, h->stream,
+                            &h->launches));
+  CK(h, osbli::launch_internal_to_abi(h->base, h->b.w, stage, 5, 0, h->stream, &h->launches));
+  CK(h, cudaMemcpyAsync(R, stage, n * sizeof(double),
                         on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, h->stream));
   CK(h, cudaStreamSynchronize(h->stream));
   return OSBLI_OK;

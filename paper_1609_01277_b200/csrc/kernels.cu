@@ -27,8 +27,15 @@ namespace osbli {
 namespace {
 
 __device__ __forceinline__ int wrapi(int i, int n) {
-  int r = i % n;
-  return r < 0 ? r + n : r;
+  // periodic index: one conditional shift covers every tile halo when n exceeds
+  // the stencil reach; the modulo only runs for grids smaller than that
+  if (i < 0) i += n;
+  else if (i >= n) i -= n;
+  if ((unsigned)i >= (unsigned)n) {
+    i %= n;
+    if (i < 0) i += n;
+  }
+  return i;
 }
 
 __device__ __forceinline__ size_t qplane(const KParams &p, int z) {
@@ -41,13 +48,10 @@ __device__ __forceinline__ int zread(const KParams &p, int z) {
   return max(-p.G, min(z, p.nz - 1 + p.G));
 }
 
-// 8-byte asynchronous global -> shared copy (LDGSTS), completed by cp_async_wait_all
+// 8-byte asynchronous global -> shared copy (LDGSTS); completed with cp.async.wait_group
 __device__ __forceinline__ void cp_async8(double *smem, const double *gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
 
 #include "zpass.cuh"
@@ -164,7 +168,7 @@ __global__ void internal_to_abi_kernel(const KParams p, const double *__restrict
 }
 
 template <int M>
-cudaError_t zpass_launch(const KParams &p, const double *q, double *rz, double *gz, int zb, int ze,
+cudaError_t zpass_launch(const KParams &p, const double *q, double *w, double *gz, int zb, int ze,
                          cudaStream_t s) {
   constexpr int smem = zp_smem_bytes<M>();
   static bool init = false;
@@ -182,14 +186,14 @@ cudaError_t zpass_launch(const KParams &p, const double *q, double *rz, double *
   const int seg_len = ((chunks + nseg - 1) / nseg) * ZP_TZ;
   nseg = (ze - zb + seg_len - 1) / seg_len;
   dim3 grid(gx, gy, nseg);
-  zpass_kernel<M><<<grid, ZP_THREADS, smem, s>>>(p, q, rz, gz, zb, ze, seg_len);
+  zpass_kernel<M><<<grid, ZP_THREADS, smem, s>>>(p, q, w, gz, zb, ze, seg_len);
   return cudaGetLastError();
 }
 
 template <int M>
 cudaError_t xypass_launch(const KParams &p, const double *q, double *qout, double *w,
-                          const double *rz, const double *gz, double *rout, unsigned int *flag,
-                          int zb, int ze, cudaStream_t s) {
+                          const double *gz, double *rout, unsigned int *flag, int zb, int ze,
+                          cudaStream_t s) {
   constexpr int smem = xy_smem_bytes<M>();
   static bool init = false;
   if (!init) {
@@ -199,7 +203,7 @@ cudaError_t xypass_launch(const KParams &p, const double *q, double *qout, doubl
     init = true;
   }
   dim3 grid((p.nx + XY_TX - 1) / XY_TX, (p.ny + XY_TY - 1) / XY_TY, ze - zb);
-  xypass_kernel<M><<<grid, XY_THREADS, smem, s>>>(p, q, qout, w, rz, gz, rout, flag, zb);
+  xypass_kernel<M><<<grid, XY_THREADS, smem, s>>>(p, q, qout, w, gz, rout, flag, zb);
   return cudaGetLastError();
 }
 
@@ -230,11 +234,11 @@ int grid1d(size_t n) {
     default: return cudaErrorInvalidValue; \
   }
 
-cudaError_t launch_zpass(const KParams &p, const double *q_in, double *rz, double *gz, int zb,
+cudaError_t launch_zpass(const KParams &p, const double *q_in, double *w, double *gz, int zb,
                          int ze, cudaStream_t s, long long *launches) {
   if (ze <= zb) return cudaSuccess;
   ++*launches;
-#define ZCALL(MM) zpass_launch<MM>(p, q_in, rz, gz, zb, ze, s)
+#define ZCALL(MM) zpass_launch<MM>(p, q_in, w, gz, zb, ze, s)
   switch (p.m) {
     case 1: return ZCALL(1);
     case 2: return ZCALL(2);
@@ -248,11 +252,11 @@ cudaError_t launch_zpass(const KParams &p, const double *q_in, double *rz, doubl
 }
 
 cudaError_t launch_xypass(const KParams &p, const double *q_in, double *q_out, double *w,
-                          const double *rz, const double *gz, double *r_out, unsigned int *flag,
+                          const double *gz, double *r_out, unsigned int *flag,
                           int zb, int ze, cudaStream_t s, long long *launches) {
   if (ze <= zb) return cudaSuccess;
   ++*launches;
-#define XCALL(MM) xypass_launch<MM>(p, q_in, q_out, w, rz, gz, r_out, flag, zb, ze, s)
+#define XCALL(MM) xypass_launch<MM>(p, q_in, q_out, w, gz, r_out, flag, zb, ze, s)
   switch (p.m) {
     case 1: return XCALL(1);
     case 2: return XCALL(2);
@@ -266,11 +270,11 @@ cudaError_t launch_xypass(const KParams &p, const double *q_in, double *q_out, d
 }
 
 cudaError_t launch_stage(const KParams &p, const double *q_in, double *q_out, double *w,
-                         double *rz, double *gz, double *r_out, unsigned int *flag,
-                         cudaStream_t s, long long *launches) {
-  cudaError_t e = launch_zpass(p, q_in, rz, gz, 0, p.nz, s, launches);
+                         double *gz, double *r_out, unsigned int *flag, cudaStream_t s,
+                         long long *launches) {
+  cudaError_t e = launch_zpass(p, q_in, w, gz, 0, p.nz, s, launches);
   if (e != cudaSuccess) return e;
-  return launch_xypass(p, q_in, q_out, w, rz, gz, r_out, flag, 0, p.nz, s, launches);
+  return launch_xypass(p, q_in, q_out, w, gz, r_out, flag, 0, p.nz, s, launches);
 }
 
 cudaError_t launch_diagnostics(const KParams &p, const double *q_in, double *scratch,

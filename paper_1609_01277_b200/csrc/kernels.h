@@ -24,29 +24,29 @@ struct KParams {
 };
 
 // Device buffers of one handle.  Q buffers: [nz + 2G][5][ny][nx] (plane-major,
-// ghost planes at both z ends); W, Rz: [nz][5][ny][nx]; Gz: [nz][3][ny][nx].
+// ghost planes at both z ends); W: [nz][5][ny][nx]; Gz: [nz][3][ny][nx].
 struct Bufs {
   double *q[2];
   double *w;
-  double *rz;
   double *gz;
   unsigned int *flag;  // non-finite flag (device)
   double *diag_part;   // [nz][3] per-plane partial sums (device)
 };
 
-// Launch one stage: zpass(Q_in) -> Rz, Gz ; xypass -> W, Q_out (or R_out if non-null).
-// R_out (optional) is [nz][5][ny][nx].
+// Launch one stage: zpass(Q_in) -> W' = A W + dt Rz, Gz ; xypass -> W = W' + dt R_xy,
+// Q_out = Q_in + B W (or, if r_out is non-null, r_out = W' + dt R_xy with the
+// caller passing A = 0, dt = 1: the residual).  r_out is [nz][5][ny][nx].
 cudaError_t launch_stage(const KParams &p, const double *q_in, double *q_out, double *w,
-                         double *rz, double *gz, double *r_out, unsigned int *flag,
-                         cudaStream_t s, long long *launches);
+                         double *gz, double *r_out, unsigned int *flag, cudaStream_t s,
+                         long long *launches);
 
 // z-pass restricted to planes [z_begin, z_end) (for boundary-first overlap).
-cudaError_t launch_zpass(const KParams &p, const double *q_in, double *rz, double *gz,
+cudaError_t launch_zpass(const KParams &p, const double *q_in, double *w, double *gz,
                          int z_begin, int z_end, cudaStream_t s, long long *launches);
 // xy-pass restricted to planes [z_begin, z_end).
 cudaError_t launch_xypass(const KParams &p, const double *q_in, double *q_out, double *w,
-                          const double *rz, const double *gz, double *r_out, unsigned int *flag,
-                          int z_begin, int z_end, cudaStream_t s, long long *launches);
+                          const double *gz, double *r_out, unsigned int *flag, int z_begin,
+                          int z_end, cudaStream_t s, long long *launches);
 
 // Per-plane diagnostics partial sums [nz][3] (E_k, enstrophy, dissipation sums).
 // scratch: >= 3*nx*ny*nz doubles (velocity).

@@ -13,7 +13,8 @@
 // keep a moderate register footprint.
 //   phase X  : x-derivatives of tile rows (A, B) + g00, g10 on the halo rows (ext)
 //   phase Y  : y-derivatives (A, B), combined with phase-X partials
-//   epilogue : R = A + B + Rz, low-storage RK stage update
+//   epilogue : W <- W' + dt (A + B), Q' <- Q + B W  (low-storage RK, P:123, P:164;
+//              W' = A W + dt Rz was written by the z-pass)
 constexpr int XY_TX = 32;
 constexpr int XY_TY = 16;
 constexpr int XY_RX = 4;
@@ -32,13 +33,13 @@ struct XYGeom {
   static constexpr int NPT = TP * XY_TY;        // tile points (padded)
   static constexpr int EXT = TP * HY;           // g00 / g10 on the y-extended tile
   static constexpr int W = 4 + 2 * M;           // window length (RX = RY = 4)
-  // layout (doubles): fields | E0 | E1 | XA[5] | XB[5] | PF[10] (prefetched Rz, W)
+  // layout (doubles): fields | E0 | E1 | XA[5] | XB[5] | PF[5] (prefetched W')
   static constexpr int OFF_E0 = XY_NF * FSZ;
   static constexpr int OFF_E1 = OFF_E0 + EXT;
   static constexpr int OFF_XA = OFF_E1 + EXT;
   static constexpr int OFF_XB = OFF_XA + 5 * NPT;
   static constexpr int OFF_PF = OFF_XB + 5 * NPT;
-  static constexpr int TOTAL = OFF_PF + 10 * XY_TX * XY_TY;
+  static constexpr int TOTAL = OFF_PF + 5 * XY_TX * XY_TY;
   static constexpr int BYTES = TOTAL * (int)sizeof(double);
 };
 
@@ -60,20 +61,28 @@ __device__ __forceinline__ void ldwin(const double *base, int st, double (&v)[W]
 
 template <int M, int W>
 __device__ __forceinline__ double wd1(const KParams &p, const double (&v)[W], int j) {
-  double s = 0.0;
+  // two interleaved partial sums halve the dependent FMA chain
+  double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-  for (int k = 1; k <= M; ++k) s = fma(p.a[k - 1], v[j + M + k] - v[j + M - k], s);
-  return s;
+  for (int k = 1; k <= M; ++k) {
+    if (k & 1) s0 = fma(p.a[k - 1], v[j + M + k] - v[j + M - k], s0);
+    else s1 = fma(p.a[k - 1], v[j + M + k] - v[j + M - k], s1);
+  }
+  return s0 + s1;
 }
 
 // second derivative, exactly zero on a constant window: sum b_k ((f+ + f-) - 2 f)
 template <int M, int W>
 __device__ __forceinline__ double wd2(const KParams &p, const double (&v)[W], int j) {
   const double c = v[j + M];
-  double s = 0.0;
+  double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-  for (int k = 1; k <= M; ++k) s = fma(p.b[k], fma(-2.0, c, v[j + M + k] + v[j + M - k]), s);
-  return s;
+  for (int k = 1; k <= M; ++k) {
+    const double t = fma(-2.0, c, v[j + M + k] + v[j + M - k]);
+    if (k & 1) s0 = fma(p.b[k], t, s0);
+    else s1 = fma(p.b[k], t, s1);
+  }
+  return s0 + s1;
 }
 
 // Velocity group, one direction (DIR 0 = x: phase X, DIR 1 = y: phase Y).
@@ -174,8 +183,8 @@ __device__ __forceinline__ void conservative_dir(const KParams &p, const double 
 template <int M>
 __global__ void __launch_bounds__(XY_THREADS, 1)
     xypass_kernel(const KParams p, const double *__restrict__ q, double *__restrict__ qout,
-                  double *__restrict__ w, const double *__restrict__ rz,
-                  const double *__restrict__ gz, double *__restrict__ rout,
+                  double *__restrict__ w, const double *__restrict__ gz,
+                  double *__restrict__ rout,
                   unsigned int *__restrict__ flag, int z_begin) {
   using Gm = XYGeom<M>;
   constexpr int HX = Gm::HX, HY = Gm::HY, PX = Gm::PX, FSZ = Gm::FSZ, NPT = Gm::NPT;
@@ -189,8 +198,8 @@ __global__ void __launch_bounds__(XY_THREADS, 1)
   const double *qp = q + qplane(p, z);
   const double *gp = gz + (size_t)z * 3 * FS;
 
-  // ---- prefetch the epilogue operands (z-pass partial residual Rz, RK register W)
-  //      asynchronously so that their latency hides behind phases X and Y
+  // ---- prefetch the epilogue operand W' (= A W + dt Rz, from the z-pass)
+  //      asynchronously so that its latency hides behind phases X and Y
   double *PF = S + Gm::OFF_PF;
   for (int lin = tid; lin < XY_TX * XY_TY; lin += XY_THREADS) {
     const int ty = lin / XY_TX, tx = lin - ty * XY_TX;
@@ -198,11 +207,7 @@ __global__ void __launch_bounds__(XY_THREADS, 1)
     if (x < p.nx && y < p.ny) {
       const size_t o = (size_t)z * 5 * FS + (size_t)y * p.nx + x;
 #pragma unroll
-      for (int f = 0; f < 5; ++f) cp_async8(PF + f * XY_TX * XY_TY + lin, rz + o + f * FS);
-      if (p.read_w && !rout) {
-#pragma unroll
-        for (int f = 0; f < 5; ++f) cp_async8(PF + (5 + f) * XY_TX * XY_TY + lin, w + o + f * FS);
-      }
+      for (int f = 0; f < 5; ++f) cp_async8(PF + f * XY_TX * XY_TY + lin, w + o + f * FS);
     }
   }
   asm volatile("cp.async.commit_group;\n" ::: "memory");
@@ -362,7 +367,8 @@ __global__ void __launch_bounds__(XY_THREADS, 1)
   }
   __syncthreads();
 
-  // ---- epilogue: R = A + B + Rz ; W <- A W + dt R ; Q' <- Q + B W  (coalesced rows)
+  // ---- epilogue: W <- W' + dt R_xy ; Q' <- Q + B W   (coalesced rows; residual mode:
+  //      A = 0, dt = 1 so that W' = Rz and R = W' + R_xy)
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
   __syncthreads();
   bool bad = false;
@@ -377,13 +383,12 @@ __global__ void __launch_bounds__(XY_THREADS, 1)
     const int fidx[5] = {XF_RHO, XF_M0, XF_M1, XF_M2, XF_E};
 #pragma unroll
     for (int f = 0; f < 5; ++f) {
-      const double Rf = XA[f * NPT + pt] + XB[f * NPT + pt] + PF[f * XY_TX * XY_TY + lin];
+      const double wn =
+          fma(p.dt, XA[f * NPT + pt] + XB[f * NPT + pt], PF[f * XY_TX * XY_TY + lin]);
       if (rout) {
-        rout[o + f * FS] = Rf;
+        rout[o + f * FS] = wn;
         continue;
       }
-      double wn = p.dt * Rf;
-      if (p.read_w) wn = fma(p.A, PF[(5 + f) * XY_TX * XY_TY + lin], wn);
       if (p.write_w) w[o + f * FS] = wn;
       const double qn = fma(p.B, wn, S[fidx[f] * FSZ + c]);
       qo[f * FS] = qn;

@@ -2,8 +2,10 @@
 //
 // Every term of the residual that differentiates along z (D_z, D_zz; the z
 // halves of the skew-symmetric terms P:271-274, the z fluxes, the z parts of
-// the viscous Laplacians P:274 and of the heat flux), written as a partial
-// residual Rz[5], plus g_i2 = D_z u_i for the xy-pass.
+// the viscous Laplacians P:274 and of the heat flux): the partial residual Rz
+// goes straight into the low-storage register, W' = A W + dt Rz (P:123,
+// P:164; the xy-pass completes W <- W' + dt R_xy), plus g_i2 = D_z u_i for
+// the xy-pass.
 //
 // A CTA owns a pencil of 32 x-columns x one y-row and marches through its
 // z-range in chunks of TZ = 32 planes.  Shared memory holds a ring of
@@ -76,25 +78,33 @@ __device__ __forceinline__ void zwindow(const double *S, int f, int slot0, int l
 
 template <int M>
 __device__ __forceinline__ double d1w(const KParams &p, const double (&v)[ZP_RZ + 2 * M], int j) {
-  double s = 0.0;
+  // two interleaved partial sums halve the dependent FMA chain
+  double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-  for (int k = 1; k <= M; ++k) s = fma(p.a[k - 1], v[j + M + k] - v[j + M - k], s);
-  return s;
+  for (int k = 1; k <= M; ++k) {
+    if (k & 1) s0 = fma(p.a[k - 1], v[j + M + k] - v[j + M - k], s0);
+    else s1 = fma(p.a[k - 1], v[j + M + k] - v[j + M - k], s1);
+  }
+  return s0 + s1;
 }
 
 // exactly zero on a constant window (D-22)
 template <int M>
 __device__ __forceinline__ double d2w(const KParams &p, const double (&v)[ZP_RZ + 2 * M], int j) {
   const double c = v[j + M];
-  double s = 0.0;
+  double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-  for (int k = 1; k <= M; ++k) s = fma(p.b[k], fma(-2.0, c, v[j + M + k] + v[j + M - k]), s);
-  return s;
+  for (int k = 1; k <= M; ++k) {
+    const double t = fma(-2.0, c, v[j + M + k] + v[j + M - k]);
+    if (k & 1) s0 = fma(p.b[k], t, s0);
+    else s1 = fma(p.b[k], t, s1);
+  }
+  return s0 + s1;
 }
 
 template <int M>
 __global__ void __launch_bounds__(ZP_THREADS, 1)
-    zpass_kernel(const KParams p, const double *__restrict__ q, double *__restrict__ rz,
+    zpass_kernel(const KParams p, const double *__restrict__ q, double *__restrict__ w,
                  double *__restrict__ gz, int z_begin, int z_end, int seg_len) {
   using Zg = ZGeom<M>;
   constexpr int NR = Zg::NR;
@@ -151,6 +161,18 @@ __global__ void __launch_bounds__(ZP_THREADS, 1)
     // ---- compute chunk k: outputs z = zs + k*TZ + warp*RZ + j
     const int zl0 = k * ZP_TZ + warp * ZP_RZ;  // local index of the window's first plane
     const int slot0 = zl0 % NR;
+    // the low-storage register of the outputs: loaded now, used after the stencils
+    double wold[5][ZP_RZ];
+    {
+      const int x = x0 + lane < p.nx ? x0 + lane : xc;
+#pragma unroll
+      for (int j = 0; j < ZP_RZ; ++j) {
+        const int z = min(zs + zl0 + j, ze - 1);
+        const size_t o = (size_t)z * 5 * FS + (size_t)y * p.nx + x;
+#pragma unroll
+        for (int f = 0; f < 5; ++f) wold[f][j] = p.read_w ? w[o + f * FS] : 0.0;
+      }
+    }
     double v[ZP_RZ + 2 * M];
     double g[3][ZP_RZ], R[5][ZP_RZ], u2c[ZP_RZ];
     // velocity: g_i2 = D_z u_i, z-Laplacian parts of V_i and u_i V_i
@@ -207,7 +229,7 @@ __global__ void __launch_bounds__(ZP_THREADS, 1)
         if (z < ze) {
           const size_t o = (size_t)z * 5 * FS + (size_t)y * p.nx + x;
 #pragma unroll
-          for (int f = 0; f < 5; ++f) rz[o + f * FS] = R[f][j];
+          for (int f = 0; f < 5; ++f) w[o + f * FS] = fma(p.A, wold[f][j], p.dt * R[f][j]);
           const size_t og = (size_t)z * 3 * FS + (size_t)y * p.nx + x;
 #pragma unroll
           for (int i = 0; i < 3; ++i) gz[og + i * FS] = g[i][j];

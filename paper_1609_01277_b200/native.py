@@ -11,7 +11,8 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _ROOT = os.path.dirname(_HERE)
-_LIB_PATH = os.path.join(_HERE, "libosbli.so")
+# OSBLI_LIB selects an alternative in-tree build (kernel-variant experiments)
+_LIB_PATH = os.environ.get("OSBLI_LIB") or os.path.join(_HERE, "libosbli.so")
 _lib = None
 
 OSBLI_EULER = 0
