@@ -267,9 +267,17 @@ def main():
     avg = xy_avg if dom == "xypass" else z_avg
     fl = xyflop if dom == "xypass" else zflop
     achieved_tf = fl * per_launch_pts / (avg * 1e-3) / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "kernel_traffic.json")
+    if os.path.exists(tpath):
+        tj = json.load(open(tpath)).get(f"{args.config}:{dom}")
+        traffic = tj["dram_bytes_per_launch"] if tj else None
     roof = {
         "kernel": dom, "bound": "alu", "achieved": achieved_tf, "peak": fp64_peak,
-        "unit": "TFLOP/s", "frac": achieved_tf / fp64_peak, "traffic": None,
+        "unit": "TFLOP/s", "frac": achieved_tf / fp64_peak, "traffic": traffic,
+        "traffic_unit": "bytes per launch (ncu dram__bytes_read.sum + dram__bytes_write.sum, "
+                        "profiles/kernel_traffic.json)",
+        "algorithmic_bytes_per_launch": (xyb if dom == "xypass" else zb) / 3 * per_launch_pts,
         "peak_source": f"FP64 = 148 SMs x 64 lanes x 2 flop x {fmax:.0f} MHz (guide unit counts; DESIGN.md §5)",
         "flops_per_point": fl, "avg_launch_ms": avg,
         "share_of_step": (xyms if dom == "xypass" else zms) / ms if ms > 0 else None,

@@ -6,10 +6,11 @@ is 5 fields x fp64 over three field-sets: stage 1 reads Q, writes Q' and W
 Q' (120 B) — 400 B per point-step; forward Euler 80 B.
 
 Our two-kernel stage adds an on-HBM hand-off between the z-pass and the
-xy-pass (partial residual Rz, 5 doubles, and g_i2, 3 doubles: written once,
-read once): 128 B per point-stage.  `kernel_bytes` gives each kernel's own
-algorithmic traffic in this design (every operand read once and every result
-written once; halo re-reads are not counted, they should hit L2).
+xy-pass: the z-pass writes W' = A W + dt Rz (the low-storage register with
+the z-part of the residual folded in) and g_i2 = D_z u_i (3 doubles); the
+xy-pass reads them.  `kernel_bytes` gives each kernel's own algorithmic
+traffic in this design (every operand read once and every result written
+once; halo re-reads are not counted, they should hit L2).
 
 FP64 flops (FMA = 2): counted from the discrete operators, one evaluation per
 point (no halo recomputation):
@@ -25,13 +26,10 @@ COMPULSORY_BYTES_EULER = 80.0
 
 def kernel_bytes(stage: int, scheme: int = 1):
     """(zpass_bytes, xypass_bytes) per point for RK3 stage 0/1/2 (Euler: stage 0, scheme 0)."""
-    z = 40.0 + 40.0 + 24.0  # read Q; write Rz, g_i2
-    xy = 40.0 + 40.0 + 24.0 + 40.0  # read Q, Rz, g_i2; write Q'
-    if scheme == 1:
-        if stage > 0:
-            xy += 40.0  # read W
-        if stage < 2:
-            xy += 40.0  # write W
+    read_w = scheme == 1 and stage > 0
+    write_w = scheme == 1 and stage < 2
+    z = 40.0 + (40.0 if read_w else 0.0) + 40.0 + 24.0  # read Q (and W); write W', g_i2
+    xy = 40.0 + 24.0 + 40.0 + 40.0 + (40.0 if write_w else 0.0)  # read Q, g, W'; write Q' (and W)
     return z, xy
 
 
