@@ -49,6 +49,10 @@ struct osbli_ctx {
   KParams base{};
   // loopback transport (one GPU, several slabs): the group of sibling handles
   struct LoopGroup *loop = nullptr;
+  // NCCL overlap: ghost exchange on comm_stream, ordered by events
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_qready = nullptr;  // boundary planes of the current Q are written
+  cudaEvent_t ev_ghost = nullptr;   // ghost planes of the current Q have arrived
   // kernel timing instrumentation: events[3*i..3*i+2] bracket stage i's two kernels
   bool timing = false;
   std::vector<cudaEvent_t> events;
@@ -241,8 +245,9 @@ void ghost_plan(int rank, int nranks, int nzl, int m, int plan[8]) {
 // z ghost planes of Q buffer `q` from the neighbouring slabs, over NCCL
 // (one process per GPU) or by device copies between sibling handles
 // (loopback transport on one GPU).
-int exchange_ghosts(osbli_ctx *h, double *q) {
+int exchange_ghosts(osbli_ctx *h, double *q, cudaStream_t st = nullptr) {
   if (h->nranks == 1) return OSBLI_OK;
+  if (!st) st = h->stream;
   const int G = h->m;
   const size_t plane = 5 * (size_t)h->nx * h->ny;
   const size_t cnt = (size_t)G * plane;
@@ -252,8 +257,8 @@ int exchange_ghosts(osbli_ctx *h, double *q) {
   if (h->comm) {
     NK(h, ncclGroupStart());
     for (int t = 0; t < 2; ++t) {
-      NK(h, ncclSend(at(q, plan[4 * t + 1]), cnt, ncclDouble, plan[4 * t + 0], h->comm, h->stream));
-      NK(h, ncclRecv(at(q, plan[4 * t + 3]), cnt, ncclDouble, plan[4 * t + 2], h->comm, h->stream));
+      NK(h, ncclSend(at(q, plan[4 * t + 1]), cnt, ncclDouble, plan[4 * t + 0], h->comm, st));
+      NK(h, ncclRecv(at(q, plan[4 * t + 3]), cnt, ncclDouble, plan[4 * t + 2], h->comm, st));
     }
     NK(h, ncclGroupEnd());
     return OSBLI_OK;
@@ -266,7 +271,7 @@ int exchange_ghosts(osbli_ctx *h, double *q) {
       int splan[8];
       ghost_plan(src->rank, src->nranks, src->nz, G, splan);
       CK(h, cudaMemcpyAsync(at(q, plan[4 * t + 3]), at(src->b.q[src->cur], splan[4 * t + 1]),
-                            cnt * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+                            cnt * sizeof(double), cudaMemcpyDeviceToDevice, st));
     }
     return OSBLI_OK;
   }
@@ -357,6 +362,12 @@ int osbli_create_dist(int nx, int ny, int nz, int order, double dx, double dt, d
                cudaSuccess) {
       h->err = "device allocation failed";
       r = OSBLI_E_NOMEM;
+    } else if (cudaStreamCreateWithFlags(&h->comm_stream, cudaStreamNonBlocking) != cudaSuccess ||
+               cudaEventCreateWithFlags(&h->ev_qready, cudaEventDisableTiming) != cudaSuccess ||
+               cudaEventCreateWithFlags(&h->ev_ghost, cudaEventDisableTiming) != cudaSuccess ||
+               cudaEventRecord(h->ev_qready, h->stream) != cudaSuccess) {
+      h->err = "stream/event creation failed";
+      r = OSBLI_E_CUDA;
     }
   }
   if (r != OSBLI_OK) {
@@ -398,6 +409,7 @@ int osbli_set_state(osbli_ctx *h, const double *q, int on_device) {
   CK(h, cudaMemcpyAsync(stage, q, n * sizeof(double),
                         on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, h->stream));
   CK(h, osbli::launch_abi_to_internal(h->base, stage, h->b.q[h->cur], h->stream, &h->launches));
+  if (h->ev_qready) CK(h, cudaEventRecord(h->ev_qready, h->stream));
   CK(h, cudaMemsetAsync(h->b.flag, 0, sizeof(unsigned int), h->stream));
   CK(h, cudaStreamSynchronize(h->stream));
   h->step_count = 0;
@@ -436,10 +448,6 @@ int run_stage(osbli_ctx *h, int s, bool exchange = true) {
     p.write_w = 0;
   }
   double *qin = h->b.q[h->cur], *qout = h->b.q[h->cur ^ 1];
-  if (exchange) {
-    int r = exchange_ghosts(h, qin);
-    if (r) return r;
-  }
   cudaEvent_t *ev = nullptr;
   if (h->timing) {
     if (h->ev_used + 3 > h->events.size()) {
@@ -451,12 +459,47 @@ int run_stage(osbli_ctx *h, int s, bool exchange = true) {
     }
     ev = &h->events[h->ev_used];
     h->ev_used += 3;
-    CK(h, cudaEventRecord(ev[0], h->stream));
   }
-  CK(h, osbli::launch_zpass(p, qin, h->b.w, h->b.gz, 0, h->nz, h->stream, &h->launches));
+  if (h->nranks == 1) {
+    if (ev) CK(h, cudaEventRecord(ev[0], h->stream));
+    CK(h, osbli::launch_zpass(p, qin, h->b.w, h->b.gz, 0, h->nz, h->stream, &h->launches));
+    if (ev) CK(h, cudaEventRecord(ev[1], h->stream));
+    CK(h, osbli::launch_xypass(p, qin, qout, h->b.w, h->b.gz, nullptr, h->b.flag, 0, h->nz,
+                               h->stream, &h->launches));
+    if (ev) CK(h, cudaEventRecord(ev[2], h->stream));
+    h->cur ^= 1;
+    return OSBLI_OK;
+  }
+  // Slab decomposition, boundary first: only the z-pass of the m planes next to
+  // each slab face reads ghost planes.  The exchange of Q's boundary planes runs
+  // on the comm stream while the interior z-pass runs; the xy-pass writes the
+  // boundary planes of Q' first so that the next stage's exchange overlaps the
+  // interior xy-pass.
+  const int m = h->m;
+  const int lo = m < h->nz ? m : h->nz;            // [0, lo): low boundary planes
+  const int hi = h->nz - m > lo ? h->nz - m : lo;  // [hi, nz): high boundary planes
+  if (h->comm) {
+    CK(h, cudaStreamWaitEvent(h->comm_stream, h->ev_qready, 0));
+    int r = exchange_ghosts(h, qin, h->comm_stream);
+    if (r) return r;
+    CK(h, cudaEventRecord(h->ev_ghost, h->comm_stream));
+  } else if (exchange) {
+    int r = exchange_ghosts(h, qin);
+    if (r) return r;
+  }
+  if (ev) CK(h, cudaEventRecord(ev[0], h->stream));
+  CK(h, osbli::launch_zpass(p, qin, h->b.w, h->b.gz, lo, hi, h->stream, &h->launches));
+  if (h->comm) CK(h, cudaStreamWaitEvent(h->stream, h->ev_ghost, 0));
+  CK(h, osbli::launch_zpass(p, qin, h->b.w, h->b.gz, 0, lo, h->stream, &h->launches));
+  CK(h, osbli::launch_zpass(p, qin, h->b.w, h->b.gz, hi, h->nz, h->stream, &h->launches));
   if (ev) CK(h, cudaEventRecord(ev[1], h->stream));
-  CK(h, osbli::launch_xypass(p, qin, qout, h->b.w, h->b.gz, nullptr, h->b.flag, 0, h->nz,
+  CK(h, osbli::launch_xypass(p, qin, qout, h->b.w, h->b.gz, nullptr, h->b.flag, 0, lo, h->stream,
+                             &h->launches));
+  CK(h, osbli::launch_xypass(p, qin, qout, h->b.w, h->b.gz, nullptr, h->b.flag, hi, h->nz,
                              h->stream, &h->launches));
+  if (h->comm) CK(h, cudaEventRecord(h->ev_qready, h->stream));
+  CK(h, osbli::launch_xypass(p, qin, qout, h->b.w, h->b.gz, nullptr, h->b.flag, lo, hi, h->stream,
+                             &h->launches));
   if (ev) CK(h, cudaEventRecord(ev[2], h->stream));
   h->cur ^= 1;
   return OSBLI_OK;
@@ -702,7 +745,11 @@ const char *osbli_last_error(const osbli_ctx *h) {
 void osbli_destroy(osbli_ctx *h) {
   if (!h) return;
   if (h->stream) cudaStreamSynchronize(h->stream);
+  if (h->comm_stream) cudaStreamSynchronize(h->comm_stream);
   if (h->comm) ncclCommDestroy(h->comm);
+  if (h->comm_stream) cudaStreamDestroy(h->comm_stream);
+  if (h->ev_qready) cudaEventDestroy(h->ev_qready);
+  if (h->ev_ghost) cudaEventDestroy(h->ev_ghost);
   for (auto e : h->events) cudaEventDestroy(e);
   free_all(h);
   LoopGroup *g = h->loop;
