@@ -23,4 +23,6 @@ from .core import (  # noqa: F401
     step,
     diagnostics,
     run_series,
+    scalar_residual,
+    scalar_step,
 )

@@ -73,6 +73,9 @@ def _L():
         _lib.oracle_step.argtypes = [P, dp, ctypes.c_int, ctypes.c_int]
         _lib.oracle_diagnostics.argtypes = [P, dp, dp]
         _lib.oracle_run_series.argtypes = [P, dp, ctypes.c_int, ctypes.c_int, dp]
+        _lib.oracle_scalar_residual.argtypes = [P, dp, ctypes.c_double, dp, dp, dp]
+        _lib.oracle_scalar_step.argtypes = [P, dp, ctypes.c_double, dp, dp, ctypes.c_int,
+                                            ctypes.c_int]
     return _lib
 
 
@@ -135,6 +138,31 @@ def run_series(p: OracleParams, Q: np.ndarray, scheme: int, nsteps: int):
     if _L().oracle_run_series(ctypes.byref(p.c()), _dp(Qn), scheme, nsteps, _dp(series)):
         raise ValueError("bad run_series arguments")
     return series, Qn
+
+
+def _u3(u):
+    return (ctypes.c_double * 3)(*[float(v) for v in u])
+
+
+def scalar_residual(p: OracleParams, u, k: float, phi: np.ndarray, S=None) -> np.ndarray:
+    """R = -d/dx_j(phi u_j) + k d2 phi/dx_j^2 - S for phi [nz][ny][nx]."""
+    phi = np.ascontiguousarray(phi, dtype=np.float64).reshape(p.nz, p.ny, p.nx)
+    Sc = None if S is None else np.ascontiguousarray(S, dtype=np.float64).reshape(phi.shape)
+    Sp = None if Sc is None else _dp(Sc)
+    R = np.empty_like(phi)
+    if _L().oracle_scalar_residual(ctypes.byref(p.c()), _u3(u), float(k), _dp(phi), Sp, _dp(R)):
+        raise ValueError("bad scalar residual arguments")
+    return R
+
+
+def scalar_step(p: OracleParams, u, k: float, phi: np.ndarray, scheme: int, nsteps: int, S=None):
+    """phi advanced by nsteps (0 = Euler, 1 = RK3); input untouched."""
+    ph = np.array(phi, dtype=np.float64, order="C").reshape(p.nz, p.ny, p.nx).copy()
+    Sc = None if S is None else np.ascontiguousarray(S, dtype=np.float64).reshape(ph.shape)
+    Sp = None if Sc is None else _dp(Sc)
+    if _L().oracle_scalar_step(ctypes.byref(p.c()), _u3(u), float(k), Sp, _dp(ph), scheme, nsteps):
+        raise ValueError("bad scalar step arguments")
+    return ph
 
 
 def is_inviscid(Re: float) -> bool:

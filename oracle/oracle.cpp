@@ -21,7 +21,10 @@
 //     a fully periodic grid;
 //   * forward Euler and the 3-stage low-storage RK3 (tableau D-1);
 //   * the kinetic-energy / enstrophy integrals and the viscous
-//     dissipation rate (D-12).
+//     dissipation rate (D-12);
+//   * the scalar advection-diffusion equation of the paper's verification
+//     cases (1D wave, 2D method of manufactured solutions) with an
+//     optional steady source term.
 //
 // The code follows the paper's structure: "formula" work arrays (u_i, p, T)
 // are evaluated first, then the inner derivatives of nested
@@ -509,6 +512,62 @@ int oracle_run_series(const oracle_params* P, double* Q, int scheme, int nsteps,
   for (int n = 1; n <= nsteps; ++n) {
     if (oracle_step(P, Q, scheme, 1) != 0) return -1;
     if (oracle_diagnostics(P, Q, series + 3 * n) != 0) return -1;
+  }
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Scalar advection-diffusion of the paper's verification cases:
+//   d phi/dt + d/dx_j [ phi u_j - k d phi/dx_j ] + S = 0
+// with constant u_j and k; the 1D wave is u = (c,0,0), k = 0, S = 0.
+// Conservative derivative of the product phi u_j (Conservative), the
+// Laplacian by the second-derivative stencil (P:274's rule), S optional.
+// ---------------------------------------------------------------------------
+static void scalar_residual(const Grid &G, const double u[3], double kd, const double *phi,
+                            const double *S, double *R) {
+  std::vector<double> uj[3];
+  for (int j = 0; j < 3; ++j) uj[j].assign(G.npts(), u[j]);
+  for (int k = 0; k < G.n[2]; ++k)
+    for (int jy = 0; jy < G.n[1]; ++jy)
+      for (int ix = 0; ix < G.n[0]; ++ix) {
+        const size_t q = G.idx(ix, jy, k);
+        double adv = 0.0, lap = 0.0;
+        for (int j = 0; j < 3; ++j) {
+          adv += D1prod(G, phi, uj[j].data(), ix, jy, k, j);
+          lap += D2(G, phi, ix, jy, k, j);
+        }
+        R[q] = -adv + kd * lap - (S ? S[q] : 0.0);
+      }
+}
+
+int oracle_scalar_residual(const oracle_params *P, const double *u3, double kd, const double *phi,
+                           const double *S, double *R) {
+  Grid G;
+  if (!make_grid(P, G) || !u3 || !phi || !R) return -1;
+  scalar_residual(G, u3, kd, phi, S, R);
+  return 0;
+}
+
+// scheme 0 = forward Euler, 1 = RK3 (2N, D-1); phi advanced in place.
+int oracle_scalar_step(const oracle_params *P, const double *u3, double kd, const double *S,
+                       double *phi, int scheme, int nsteps) {
+  Grid G;
+  if (!make_grid(P, G) || !u3 || !phi || (scheme != 0 && scheme != 1) || nsteps < 0) return -1;
+  const size_t N = G.npts();
+  std::vector<double> R(N), W(N, 0.0);
+  for (int it = 0; it < nsteps; ++it) {
+    if (scheme == 0) {
+      scalar_residual(G, u3, kd, phi, S, R.data());
+      for (size_t q = 0; q < N; ++q) phi[q] = phi[q] + P->dt * R[q];
+    } else {
+      for (int s = 0; s < 3; ++s) {
+        scalar_residual(G, u3, kd, phi, S, R.data());
+        for (size_t q = 0; q < N; ++q) {
+          W[q] = RK_A[s] * W[q] + P->dt * R[q];
+          phi[q] = phi[q] + RK_B[s] * W[q];
+        }
+      }
+    }
   }
   return 0;
 }

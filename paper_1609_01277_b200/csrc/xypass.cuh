@@ -214,7 +214,59 @@ __global__ void __launch_bounds__(XY_THREADS, 1)
 
   // ---- stage the tile + halo: conservative state, p, 1/rho, g_i2.  All global
   //      loads of a thread are issued before the first shared store (MLP).
-  {
+  auto stage_point = [&](int s, const double *v) {
+    const double rho = v[0], m0 = v[1], m1 = v[2], m2 = v[3], e = v[4];
+    const double r = 1.0 / rho;
+    S[XF_RHO * FSZ + s] = rho;
+    S[XF_M0 * FSZ + s] = m0;
+    S[XF_M1 * FSZ + s] = m1;
+    S[XF_M2 * FSZ + s] = m2;
+    S[XF_E * FSZ + s] = e;
+    S[XF_P * FSZ + s] = p.gm1 * (e - 0.5 * r * (m0 * m0 + m1 * m1 + m2 * m2));
+    S[XF_R * FSZ + s] = r;
+    S[XF_G02 * FSZ + s] = v[5];
+    S[XF_G12 * FSZ + s] = v[6];
+    S[XF_G22 * FSZ + s] = v[7];
+  };
+  bool paired = false;
+  if constexpr (M % 2 == 0) paired = (p.nx % 2 == 0);
+  if (paired) {
+    // m and nx even: x0 - m + hx is even for even hx and never straddles the
+    // periodic seam, so two neighbouring columns come in one 16-byte load
+    constexpr int NP2 = HX / 2 * HY;
+    constexpr int NIT = (NP2 + XY_THREADS - 1) / XY_THREADS;
+    double2 raw[NIT][8];
+#pragma unroll
+    for (int it = 0; it < NIT; ++it) {
+      const int idx = tid + it * XY_THREADS;
+      if (idx < NP2) {
+        const int hy = idx / (HX / 2), hx = 2 * (idx - hy * (HX / 2));
+        const int x = wrapi(x0 - M + hx, p.nx), y = wrapi(y0 - M + hy, p.ny);
+        const size_t off = (size_t)y * p.nx + x;
+#pragma unroll
+        for (int f = 0; f < 5; ++f)
+          raw[it][f] = __ldg(reinterpret_cast<const double2 *>(qp + f * FS + off));
+#pragma unroll
+        for (int f = 0; f < 3; ++f)
+          raw[it][5 + f] = __ldg(reinterpret_cast<const double2 *>(gp + f * FS + off));
+      }
+    }
+#pragma unroll
+    for (int it = 0; it < NIT; ++it) {
+      const int idx = tid + it * XY_THREADS;
+      if (idx < NP2) {
+        const int hy = idx / (HX / 2), hx = 2 * (idx - hy * (HX / 2));
+        double a[8], b[8];
+#pragma unroll
+        for (int f = 0; f < 8; ++f) {
+          a[f] = raw[it][f].x;
+          b[f] = raw[it][f].y;
+        }
+        stage_point(hy * PX + hx, a);
+        stage_point(hy * PX + hx + 1, b);
+      }
+    }
+  } else {
     constexpr int NIT = (HX * HY + XY_THREADS - 1) / XY_THREADS;
     double raw[NIT][8];
 #pragma unroll
@@ -235,21 +287,7 @@ __global__ void __launch_bounds__(XY_THREADS, 1)
       const int idx = tid + it * XY_THREADS;
       if (idx < HX * HY) {
         const int hy = idx / HX, hx = idx - hy * HX;
-        const double rho = raw[it][0], m0 = raw[it][1], m1 = raw[it][2], m2 = raw[it][3],
-                     e = raw[it][4];
-        const double r = 1.0 / rho;
-        const double pr = p.gm1 * (e - 0.5 * r * (m0 * m0 + m1 * m1 + m2 * m2));
-        const int s = hy * PX + hx;
-        S[XF_RHO * FSZ + s] = rho;
-        S[XF_M0 * FSZ + s] = m0;
-        S[XF_M1 * FSZ + s] = m1;
-        S[XF_M2 * FSZ + s] = m2;
-        S[XF_E * FSZ + s] = e;
-        S[XF_P * FSZ + s] = pr;
-        S[XF_R * FSZ + s] = r;
-        S[XF_G02 * FSZ + s] = raw[it][5];
-        S[XF_G12 * FSZ + s] = raw[it][6];
-        S[XF_G22 * FSZ + s] = raw[it][7];
+        stage_point(hy * PX + hx, raw[it]);
       }
     }
   }
