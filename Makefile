@@ -21,10 +21,16 @@ all: $(LIB) oracle/liboracle.so
 $(CSRC)/kernels.o: $(CSRC)/kernels.cu $(CSRC)/kernels.h $(wildcard $(CSRC)/*.cuh)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(CSRC)/ptxas.log || (cat $(CSRC)/ptxas.log; false)
 
-$(CSRC)/api.o: $(CSRC)/api.cpp $(CSRC)/kernels.h include/osbli.h
+$(CSRC)/api.o: $(CSRC)/api.cpp $(CSRC)/kernels.h $(CSRC)/weights.h include/osbli.h
 	$(NVCC) $(ARCH) -O2 -std=c++17 -Xcompiler -fPIC $(NCCL_INC) -x cu -c $< -o $@
 
-$(LIB): $(CSRC)/kernels.o $(CSRC)/api.o
+$(CSRC)/scalar.o: $(CSRC)/scalar.cu $(CSRC)/scalar.h
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(CSRC)/ptxas_scalar.log || (cat $(CSRC)/ptxas_scalar.log; false)
+
+$(CSRC)/scalar_api.o: $(CSRC)/scalar_api.cpp $(CSRC)/scalar.h $(CSRC)/weights.h include/osbli.h
+	$(NVCC) $(ARCH) -O2 -std=c++17 -Xcompiler -fPIC -x cu -c $< -o $@
+
+$(LIB): $(CSRC)/kernels.o $(CSRC)/api.o $(CSRC)/scalar.o $(CSRC)/scalar_api.o
 	$(NVCC) $(ARCH) -shared -o $@ $^ $(NCCL_LIB) -lcudart
 
 oracle/liboracle.so: oracle/oracle.cpp

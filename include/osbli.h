@@ -136,7 +136,14 @@ int osbli_step(osbli_ctx *h, int n);
  * every rank gets the same, decomposition-independent numbers). */
 int osbli_diagnostics(osbli_ctx *h, osbli_diag *out);
 
-/* Test hook: R(Q) of the current state, [5][nz_local][ny][nx], no update. */
+/* Steady source term S added to the right-hand side, dQ/dt = R(Q) + S (the
+ * method of manufactured solutions).  S is
+ * [5][nz_local][ny][nx] on the host or the device; NULL removes it.  The
+ * library keeps its own copy. */
+int osbli_set_source(osbli_ctx *h, const double *S, int on_device);
+
+/* Test hook: dQ/dt = R(Q) (+ S if set) of the current state,
+ * [5][nz_local][ny][nx], no update. */
 int osbli_residual(osbli_ctx *h, double *R, int on_device);
 
 /* Wait for queued work; surfaces asynchronous errors (NONFINITE, CUDA). */
@@ -160,6 +167,25 @@ const char *osbli_last_error(const osbli_ctx *h);
 const char *osbli_version(void);
 
 void osbli_destroy(osbli_ctx *h);
+
+/* ---------------------------------------------------------------------------
+ * Scalar advection-diffusion, the equation of the paper's verification cases
+ * (1D wave P:176-184, 2D manufactured solution P:195-209):
+ *     d phi/dt + d/dx_j [ phi u_j - kappa d phi/dx_j ] + S = 0
+ * with constant (u0, u1, u2) and kappa >= 0, on the same periodic grid, central
+ * differences (order 2..12), Euler or RK3.  phi and S are [nz][ny][nx] fp64.
+ * Same error codes and conventions as the NS handle. */
+typedef struct osbli_scalar osbli_scalar;
+int osbli_scalar_create(int nx, int ny, int nz, int order, double dx, double dt, double u0,
+                        double u1, double u2, double kappa, int scheme, osbli_scalar **out);
+int osbli_scalar_set_state(osbli_scalar *h, const double *phi, int on_device);
+int osbli_scalar_set_source(osbli_scalar *h, const double *S, int on_device); /* NULL: none */
+int osbli_scalar_get_state(osbli_scalar *h, double *phi, int on_device);
+int osbli_scalar_step(osbli_scalar *h, int n);
+int osbli_scalar_residual(osbli_scalar *h, double *R, int on_device); /* d phi/dt */
+int osbli_scalar_sync(osbli_scalar *h);
+const char *osbli_scalar_last_error(const osbli_scalar *h);
+void osbli_scalar_destroy(osbli_scalar *h);
 
 #ifdef __cplusplus
 }

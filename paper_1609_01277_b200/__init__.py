@@ -13,6 +13,7 @@ from .native import (  # noqa: F401
     OSBLI_RK3,
     LoopbackGroup,
     OsbliError,
+    ScalarSolver,
     Solver,
     ghost_plan,
     slab_bounds,

@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "kernels.h"
+#include "weights.h"
 
 using osbli::Bufs;
 using osbli::KParams;
@@ -39,6 +40,7 @@ struct osbli_ctx {
   Bufs b{};
   double *scratch = nullptr;  // velocity for diagnostics, [nz + 2G][3][ny][nx]
   double *nccl_part = nullptr;  // [nranks * max_nz][3] gathered plane partials
+  double *src = nullptr;        // optional source S, plane-major [nz][5][ny][nx]
   int max_nz = 0;
   int cur = 0;
   long long step_count = 0;
@@ -62,57 +64,6 @@ struct osbli_ctx {
 namespace {
 
 thread_local std::string g_create_error;
-
-struct Frac64 {
-  long long n, d;
-};
-
-long long gcdll(long long a, long long b) {
-  if (a < 0) a = -a;
-  if (b < 0) b = -b;
-  while (b) {
-    long long t = a % b;
-    a = b;
-    b = t;
-  }
-  return a;
-}
-
-long long fact(int n) {
-  long long r = 1;
-  for (int i = 2; i <= n; ++i) r *= i;
-  return r;
-}
-
-// Central-difference weights in closed form (explicit Lagrange-derivative
-// formula; exact in int64 for m <= 6):
-//   a_k = (-1)^(k+1) (m!)^2 / (k (m-k)! (m+k)!)
-//   b_k = 2 (-1)^(k+1) (m!)^2 / (k^2 (m-k)! (m+k)!),  b_0 = -2 sum_k b_k
-void weights(int m, double *a, double *b) {
-  const long long mf2 = fact(m) * fact(m);
-  std::vector<Frac64> bk;
-  for (int k = 1; k <= m; ++k) {
-    const long long sgn = (k % 2 == 1) ? 1 : -1;
-    long long n = sgn * mf2, d = (long long)k * fact(m - k) * fact(m + k);
-    long long g = gcdll(n, d);
-    a[k - 1] = (double)(n / g) / (double)(d / g);
-    long long n2 = 2 * sgn * mf2, d2 = (long long)k * k * fact(m - k) * fact(m + k);
-    g = gcdll(n2, d2);
-    bk.push_back({n2 / g, d2 / g});
-    b[k] = (double)(n2 / g) / (double)(d2 / g);
-  }
-  // b_0 exactly: sum of fractions
-  long long N = 0, D = 1;
-  for (auto &f : bk) {
-    const long long g = gcdll(D, f.d);
-    const long long L = D / g * f.d;
-    N = N * (L / D) + f.n * (L / f.d);
-    D = L;
-    const long long h = gcdll(N, D);
-    if (h > 1) { N /= h; D /= h; }
-  }
-  b[0] = -2.0 * (double)N / (double)D;
-}
 
 int fail(osbli_ctx *h, int code, const std::string &msg) {
   h->err = msg;
@@ -161,6 +112,8 @@ void free_all(osbli_ctx *h) {
   cudaFree(h->b.diag_part);
   cudaFree(h->scratch);
   cudaFree(h->nccl_part);
+  cudaFree(h->src);
+  h->src = nullptr;
   h->b = Bufs{};
   h->scratch = nullptr;
   h->nccl_part = nullptr;
@@ -203,7 +156,7 @@ int create_common(osbli_ctx *h) {
   p.zwrap = (h->nranks == 1) ? 1 : 0;
   p.m = h->m;
   double a[osbli::kMaxHalf] = {0}, b[osbli::kMaxHalf + 1] = {0};
-  weights(h->m, a, b);
+  osbli::central_weights(h->m, a, b);
   for (int k = 0; k < h->m; ++k) p.a[k] = a[k] / h->dx;
   for (int k = 0; k <= h->m; ++k) p.b[k] = b[k] / (h->dx * h->dx);
   const bool inviscid = std::isinf(h->Re);
@@ -601,6 +554,30 @@ int osbli_loopback_step(osbli_ctx **hs, int nslabs, int n) {
     }
     for (int r = 0; r < nslabs; ++r) ++hs[r]->step_count;
   }
+  return OSBLI_OK;
+}
+
+int osbli_set_source(osbli_ctx *h, const double *S, int on_device) {
+  int u = check_usable(h);
+  if (u) return u;
+  CK(h, cudaStreamSynchronize(h->stream));
+  if (!S) {
+    cudaFree(h->src);
+    h->src = nullptr;
+    h->base.src = nullptr;
+    return OSBLI_OK;
+  }
+  const size_t n = (size_t)5 * h->nz * h->nx * h->ny;
+  if (!h->src) CK(h, cudaMalloc((void **)&h->src, n * sizeof(double)));
+  // ABI layout -> plane-major (no ghost planes) through the idle ping-pong buffer
+  double *stage = h->b.q[h->cur ^ 1];
+  CK(h, cudaMemcpyAsync(stage, S, n * sizeof(double),
+                        on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, h->stream));
+  KParams p0 = h->base;
+  p0.G = 0;
+  CK(h, osbli::launch_abi_to_internal(p0, stage, h->src, h->stream, &h->launches));
+  CK(h, cudaStreamSynchronize(h->stream));
+  h->base.src = h->src;
   return OSBLI_OK;
 }
 

@@ -21,6 +21,7 @@ struct KParams {
   // stage update: W <- A W + dt R ; Q' <- Q + B W
   double A, B, dt;
   int read_w, write_w;     // A != 0 ; W needed by a later stage
+  const double *src;       // optional steady source S, [nz][5][ny][nx] (dQ/dt = R + S)
 };
 
 // Device buffers of one handle.  Q buffers: [nz + 2G][5][ny][nx] (plane-major,

@@ -1,0 +1,23 @@
+// Internal interface of the scalar advection-diffusion kernel (scalar.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+namespace osbli {
+
+struct SParams {
+  int nx, ny, nz, m;
+  double a[6];   // a_k / dx
+  double b[7];   // b_k / dx^2
+  double u[3];   // advection velocity
+  double kd;     // diffusivity
+  double A, B, dt;
+  int read_w, write_w;
+};
+
+// One stage: W <- A W + dt R(phi), out <- phi + B W; or rout <- R(phi) if rout != null.
+// src (optional) is the steady source S of d phi/dt = ... - S.  Arrays [nz][ny][nx].
+cudaError_t launch_scalar_stage(const SParams &p, const double *phi, double *out, double *w,
+                                const double *src, double *rout, unsigned int *flag,
+                                cudaStream_t s);
+
+}  // namespace osbli

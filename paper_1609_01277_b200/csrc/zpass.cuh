@@ -3,7 +3,8 @@
 // Every term of the residual that differentiates along z (D_z, D_zz; the z
 // halves of the skew-symmetric terms P:271-274, the z fluxes, the z parts of
 // the viscous Laplacians P:274 and of the heat flux): the partial residual Rz
-// goes straight into the low-storage register, W' = A W + dt Rz (P:123,
+// (plus the optional source S) goes straight into the low-storage register,
+// W' = A W + dt (Rz + S) (P:123,
 // P:164; the xy-pass completes W <- W' + dt R_xy), plus g_i2 = D_z u_i for
 // the xy-pass.
 //
@@ -229,7 +230,10 @@ __global__ void __launch_bounds__(ZP_THREADS, 1)
         if (z < ze) {
           const size_t o = (size_t)z * 5 * FS + (size_t)y * p.nx + x;
 #pragma unroll
-          for (int f = 0; f < 5; ++f) w[o + f * FS] = fma(p.A, wold[f][j], p.dt * R[f][j]);
+          for (int f = 0; f < 5; ++f) {
+            const double rf = p.src ? R[f][j] + p.src[o + f * FS] : R[f][j];
+            w[o + f * FS] = fma(p.A, wold[f][j], p.dt * rf);
+          }
           const size_t og = (size_t)z * 3 * FS + (size_t)y * p.nx + x;
 #pragma unroll
           for (int i = 0; i < 3; ++i) gz[og + i * FS] = g[i][j];

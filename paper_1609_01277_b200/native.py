@@ -79,6 +79,18 @@ def load():
                                         c_double, c_double, c_double, c_int, c_int,
                                         ctypes.POINTER(H)]
     L.osbli_loopback_step.argtypes = [ctypes.POINTER(H), c_int, c_int]
+    L.osbli_set_source.argtypes = [H, vp, c_int]
+    L.osbli_scalar_create.argtypes = [c_int, c_int, c_int, c_int, c_double, c_double, c_double,
+                                      c_double, c_double, c_double, c_int, ctypes.POINTER(H)]
+    for fn in ("osbli_scalar_set_state", "osbli_scalar_set_source", "osbli_scalar_get_state",
+               "osbli_scalar_residual"):
+        getattr(L, fn).argtypes = [H, vp, c_int]
+    L.osbli_scalar_step.argtypes = [H, c_int]
+    L.osbli_scalar_sync.argtypes = [H]
+    L.osbli_scalar_last_error.argtypes = [H]
+    L.osbli_scalar_last_error.restype = ctypes.c_char_p
+    L.osbli_scalar_destroy.argtypes = [H]
+    L.osbli_scalar_destroy.restype = None
     L.osbli_kernel_launches.argtypes = [H]
     L.osbli_kernel_launches.restype = ctypes.c_longlong
     L.osbli_last_error.argtypes = [H]
@@ -204,6 +216,16 @@ class Solver:
     def sync(self):
         self._check(self._L.osbli_sync(self._h))
 
+    def set_source(self, S):
+        """Steady source: dQ/dt = R(Q) + S (None removes it)."""
+        if S is None:
+            self._check(self._L.osbli_set_source(self._h, None, 0))
+            return
+        if tuple(S.shape) != self.shape:
+            raise ValueError(f"source shape {tuple(S.shape)} != {self.shape}")
+        p, dev = _ptr(S)
+        self._check(self._L.osbli_set_source(self._h, ctypes.c_void_p(p), dev))
+
     def set_kernel_timing(self, enable: bool):
         self._check(self._L.osbli_set_kernel_timing(self._h, 1 if enable else 0))
 
@@ -246,6 +268,67 @@ class Solver:
 
     def __exit__(self, *a):
         self.close()
+
+
+class ScalarSolver:
+    """Scalar advection-diffusion of the paper's verification cases (osbli_scalar_*):
+    d phi/dt + d/dx_j [phi u_j - kappa d phi/dx_j] + S = 0, phi [nz][ny][nx]."""
+
+    def __init__(self, nx, ny, nz, order, dx, dt, u=(0.0, 0.0, 0.0), kappa=0.0,
+                 scheme=OSBLI_RK3):
+        L = load()
+        self._L = L
+        self._h = ctypes.c_void_p()
+        rc = L.osbli_scalar_create(nx, ny, nz, order, dx, dt, float(u[0]), float(u[1]),
+                                   float(u[2]), float(kappa), scheme, ctypes.byref(self._h))
+        if rc != 0:
+            raise OsbliError(rc, L.osbli_scalar_last_error(None).decode())
+        self.shape = (nz, ny, nx)
+
+    def _check(self, rc):
+        if rc != 0:
+            raise OsbliError(rc, self._L.osbli_scalar_last_error(self._h).decode())
+
+    def _io(self, fn, a):
+        if tuple(a.shape) != self.shape:
+            raise ValueError(f"shape {tuple(a.shape)} != {self.shape}")
+        p, dev = _ptr(a)
+        self._check(fn(self._h, ctypes.c_void_p(p), dev))
+        return a
+
+    def set_state(self, phi):
+        self._io(self._L.osbli_scalar_set_state, phi)
+
+    def set_source(self, S):
+        if S is None:
+            self._check(self._L.osbli_scalar_set_source(self._h, None, 0))
+        else:
+            self._io(self._L.osbli_scalar_set_source, S)
+
+    def get_state(self, out=None):
+        return self._io(self._L.osbli_scalar_get_state,
+                        np.empty(self.shape) if out is None else out)
+
+    def residual(self, out=None):
+        return self._io(self._L.osbli_scalar_residual,
+                        np.empty(self.shape) if out is None else out)
+
+    def step(self, n=1):
+        self._check(self._L.osbli_scalar_step(self._h, int(n)))
+
+    def sync(self):
+        self._check(self._L.osbli_scalar_sync(self._h))
+
+    def close(self):
+        if self._h:
+            self._L.osbli_scalar_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class LoopbackGroup:
