@@ -79,16 +79,16 @@ def test_paper_wave_on_gpu(osbli, oracle_lib):
 
 def test_paper_mms_convergence_study_on_gpu(osbli):
     """The paper's §3.2 study on the GPU: k = 0.75, u = (1, -0.5),
-    phi_m = sin x cos y, orders 2..12, dx = pi/2 .. pi/32, Courant 0.025, T = 100.
+    phi_m = sin x cos y, orders 2..12, dx = pi/2 .. pi/32, Courant 0.02 (<= 0.025), T = 100.
     The GPU steady state equals the closed-form discrete steady state and the L2
     error falls at the nominal rate; 12th order reaches machine precision."""
-    from tests.test_oracle_scalar import MMS_K, MMS_U, mms_discrete_steady, mms_fields
+    from tests.test_oracle_scalar import MMS_COURANT, MMS_K, MMS_U, mms_discrete_steady, mms_fields
     ns = [4, 8, 16, 32, 64]
     for order in (2, 4, 6, 8, 10, 12):
         errs = []
         for n in ns:
             dx, X, Y, phi_m, S = mms_fields(n)
-            dt0 = 0.025 * dx / max(abs(MMS_U[0]), abs(MMS_U[1]))
+            dt0 = MMS_COURANT * dx / max(abs(MMS_U[0]), abs(MMS_U[1]))
             nsteps = int(math.ceil(100.0 / dt0))
             s = osbli.ScalarSolver(n, n, 1, order, dx, 100.0 / nsteps, u=MMS_U, kappa=MMS_K)
             s.set_state(np.zeros((1, n, n)))
