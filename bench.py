@@ -30,7 +30,73 @@ CONFIGS = {
     "tgv256_o12": dict(n=256, order=12, scheme=1, desc="BASELINE configs[3]: TGV 256^3 12th order RK3"),
     "tgv256_o8": dict(n=256, order=8, scheme=1, desc="BASELINE configs[4]: TGV 256^3/GPU 8th order RK3"),
     "tgv64_o4": dict(n=64, order=4, scheme=1, desc="BASELINE configs[1]: TGV 64^3 4th order RK3"),
+    # the paper's scalar verification equation in 3D
+    "scalar256_o12": dict(n=256, order=12, scheme=1, scalar=True,
+                          desc="N1: scalar advection-diffusion 256^3, 12th order RK3, "
+                               "u = (1, -0.5, 0.25), k = 0.75 (P:205 parameters)"),
 }
+
+
+def run_scalar(args, cfg):
+    """Replicas (one independent problem per rank): device-timed RK3 steps of the
+    scalar advection-diffusion solver."""
+    import numpy as np
+    import torch
+
+    import paper_1609_01277_b200 as osbli
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and not torch.distributed.is_initialized():
+        torch.distributed.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    n, order = cfg["n"], cfg["order"]
+    dx = 2 * math.pi / n
+    u, kd = (1.0, -0.5, 0.25), 0.75
+    dt = 0.02 * dx
+    s = osbli.ScalarSolver(n, n, n, order, dx, dt, u=u, kappa=kd)
+    stream = torch.cuda.Stream()
+    s.set_stream(stream.cuda_stream)
+    x = np.arange(n) * dx
+    Z, Y, X = np.meshgrid(x, x, x, indexing="ij")
+    s.set_state(np.ascontiguousarray(np.sin(X) * np.cos(Y) * np.cos(Z)))
+    for _ in range(args.warmup):
+        s.step(1)
+    s.sync()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    s.step(args.steps)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    s.sync()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    if rank != 0:
+        return
+    value = world * n ** 3 * args.steps / (ms * 1e-3)
+    peaks, src = measured_peaks()
+    bytes_step = 80.0  # phi and W round trips of the three stages (24 + 32 + 24 B)
+    achieved = value / world * bytes_step / 1e9
+    print(json.dumps({
+        "metric": "grid-point RK3 updates/s (fp64)", "value": value, "unit": "pt-steps/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg["desc"], "grid": [n] * 3, "order": order,
+                   "parallelism": f"replicas x{world}", "l2": "inputs larger than L2"},
+        "roofline": {"kernel": "scalar_stage", "bound": "hbm", "achieved": achieved,
+                     "peak": float(peaks["hbm_gbs"]), "unit": "GB/s",
+                     "frac": achieved / float(peaks["hbm_gbs"]), "traffic": None,
+                     "bytes_per_point_step": bytes_step,
+                     "timing": "CUDA events on the solver stream"},
+        "gpu_launches": 3 * args.steps,
+    }), flush=True)
 
 
 def measured_peaks():
@@ -113,16 +179,27 @@ def run_reference(args, cfg, n_glob, dx, dt):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    import numpy as np
+
     from inputs import TGV_PHYS, tgv
     from oracle import core
     ns = 24
-    p = core.OracleParams(ns, ns, ns, cfg["order"], dx, dt=dt, **TGV_PHYS)
-    Q = tgv(ns, ns, ns, dx=dx)
+    if cfg.get("scalar"):
+        dts = 0.02 * dx
+        p = core.OracleParams(ns, ns, ns, cfg["order"], dx, dt=dts)
+        x = np.arange(ns) * dx
+        Z, Y, X = np.meshgrid(x, x, x, indexing="ij")
+        Q = np.sin(X) * np.cos(Y) * np.cos(Z)
+        adv = lambda st, k: core.scalar_step(p, (1.0, -0.5, 0.25), 0.75, st, 1, k)  # noqa: E731
+    else:
+        p = core.OracleParams(ns, ns, ns, cfg["order"], dx, dt=dt, **TGV_PHYS)
+        Q = tgv(ns, ns, ns, dx=dx)
+        adv = lambda st, k: core.step(p, st, 1, k)  # noqa: E731
     for _ in range(args.warmup):
-        Q = core.step(p, Q, 1, 1)
+        Q = adv(Q, 1)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        Q = core.step(p, Q, 1, 1)
+        Q = adv(Q, 1)
     el = time.perf_counter() - t0
     rate = ns ** 3 * args.steps / el
     sample = (f"oracle RK3 on a periodic {ns}^3 TGV sample at the workload's dx/order/dt "
@@ -158,6 +235,9 @@ def main():
     dt = 3.385e-3 * 64 / n
     if args.impl == "reference":
         run_reference(args, cfg, n, dx, dt)
+        return
+    if cfg.get("scalar"):
+        run_scalar(args, cfg)
         return
 
     import numpy as np

@@ -178,6 +178,7 @@ void osbli_destroy(osbli_ctx *h);
 typedef struct osbli_scalar osbli_scalar;
 int osbli_scalar_create(int nx, int ny, int nz, int order, double dx, double dt, double u0,
                         double u1, double u2, double kappa, int scheme, osbli_scalar **out);
+int osbli_scalar_set_stream(osbli_scalar *h, void *cuda_stream); /* NULL: own stream */
 int osbli_scalar_set_state(osbli_scalar *h, const double *phi, int on_device);
 int osbli_scalar_set_source(osbli_scalar *h, const double *S, int on_device); /* NULL: none */
 int osbli_scalar_get_state(osbli_scalar *h, double *phi, int on_device);

@@ -21,7 +21,7 @@ struct osbli_scalar {
   double *src = nullptr;
   unsigned int *flag = nullptr;
   int cur = 0;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr, own_stream = nullptr;
   bool poisoned = false;
   long long steps = 0;
   std::string err;
@@ -50,7 +50,7 @@ void sfree(osbli_scalar *h) {
   cudaFree(h->w);
   cudaFree(h->src);
   cudaFree(h->flag);
-  if (h->stream) cudaStreamDestroy(h->stream);
+  if (h->own_stream) cudaStreamDestroy(h->own_stream);
 }
 
 size_t npts(const osbli_scalar *h) { return (size_t)h->nx * h->ny * h->nz; }
@@ -89,16 +89,25 @@ int osbli_scalar_create(int nx, int ny, int nz, int order, double dx, double dt,
       cudaMalloc((void **)&h->phi[1], n * sizeof(double)) != cudaSuccess ||
       cudaMalloc((void **)&h->w, n * sizeof(double)) != cudaSuccess ||
       cudaMalloc((void **)&h->flag, sizeof(unsigned int)) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaMemsetAsync(h->phi[0], 0, n * sizeof(double), h->stream) != cudaSuccess ||
-      cudaMemsetAsync(h->flag, 0, sizeof(unsigned int), h->stream) != cudaSuccess ||
-      cudaStreamSynchronize(h->stream) != cudaSuccess) {
+      cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaMemsetAsync(h->phi[0], 0, n * sizeof(double), h->own_stream) != cudaSuccess ||
+      cudaMemsetAsync(h->flag, 0, sizeof(unsigned int), h->own_stream) != cudaSuccess ||
+      cudaStreamSynchronize(h->own_stream) != cudaSuccess) {
     g_scalar_error = std::string("device setup failed: ") + cudaGetErrorString(cudaGetLastError());
     sfree(h);
     delete h;
     return OSBLI_E_NOMEM;
   }
+  h->stream = h->own_stream;
   *out = h;
+  return OSBLI_OK;
+}
+
+int osbli_scalar_set_stream(osbli_scalar *h, void *cuda_stream) {
+  if (!h) return OSBLI_E_INVAL;
+  if (h->poisoned) return OSBLI_E_STATE;
+  SCK(h, cudaStreamSynchronize(h->stream));
+  h->stream = cuda_stream ? (cudaStream_t)cuda_stream : h->own_stream;
   return OSBLI_OK;
 }
 

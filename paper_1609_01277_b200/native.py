@@ -86,6 +86,7 @@ def load():
                "osbli_scalar_residual"):
         getattr(L, fn).argtypes = [H, vp, c_int]
     L.osbli_scalar_step.argtypes = [H, c_int]
+    L.osbli_scalar_set_stream.argtypes = [H, vp]
     L.osbli_scalar_sync.argtypes = [H]
     L.osbli_scalar_last_error.argtypes = [H]
     L.osbli_scalar_last_error.restype = ctypes.c_char_p
@@ -295,6 +296,9 @@ class ScalarSolver:
         p, dev = _ptr(a)
         self._check(fn(self._h, ctypes.c_void_p(p), dev))
         return a
+
+    def set_stream(self, stream_handle):
+        self._check(self._L.osbli_scalar_set_stream(self._h, ctypes.c_void_p(stream_handle or 0)))
 
     def set_state(self, phi):
         self._io(self._L.osbli_scalar_set_state, phi)
