@@ -56,6 +56,7 @@ __device__ __forceinline__ void cp_async8(double *smem, const double *gmem) {
 
 #include "zpass.cuh"
 #include "xypass.cuh"
+#include "xypass_ws.cuh"
 
 // ------------------------------------------------------------------ diagnostics
 __global__ void velocity_kernel(const KParams p, const double *__restrict__ q,
@@ -190,10 +191,27 @@ cudaError_t zpass_launch(const KParams &p, const double *q, double *w, double *g
   return cudaGetLastError();
 }
 
+#ifndef OSBLI_XY_WS
+#define OSBLI_XY_WS 1
+#endif
 template <int M>
 cudaError_t xypass_launch(const KParams &p, const double *q, double *qout, double *w,
                           const double *gz, double *rout, unsigned int *flag, int zb, int ze,
                           cudaStream_t s) {
+#if OSBLI_XY_WS
+  constexpr int smem = ws::xy_smem_bytes<M>();
+  static bool init = false;
+  if (!init) {
+    cudaError_t e = cudaFuncSetAttribute(ws::xypass_kernel<M>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    init = true;
+  }
+  const int seg = ze - zb < ws::XY_SEG ? ze - zb : ws::XY_SEG;
+  dim3 grid((p.nx + ws::XY_TX - 1) / ws::XY_TX, (p.ny + ws::XY_TY - 1) / ws::XY_TY,
+            (ze - zb + seg - 1) / seg);
+  ws::xypass_kernel<M><<<grid, ws::XY_CTA, smem, s>>>(p, q, qout, w, gz, rout, flag, zb, ze, seg);
+#else
   constexpr int smem = xy_smem_bytes<M>();
   static bool init = false;
   if (!init) {
@@ -204,6 +222,7 @@ cudaError_t xypass_launch(const KParams &p, const double *q, double *qout, doubl
   }
   dim3 grid((p.nx + XY_TX - 1) / XY_TX, (p.ny + XY_TY - 1) / XY_TY, ze - zb);
   xypass_kernel<M><<<grid, XY_THREADS, smem, s>>>(p, q, qout, w, gz, rout, flag, zb);
+#endif
   return cudaGetLastError();
 }
 

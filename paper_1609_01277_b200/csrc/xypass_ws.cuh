@@ -1,0 +1,455 @@
+namespace ws {
+// xy-pass (included by kernels.cu inside namespace osbli::{anon}).
+//
+// A CTA owns a 32 x 16 tile of the xy-plane and marches through a segment of
+// z-planes (persistent, one CTA per SM), warp-specialised: warps 0-7 compute,
+// warps 8-11 are producers that stream the next plane into the other plane buffer
+// with cp.async while the consumers work on the current one (full/empty
+// handshake on named barriers), so the consumer warps spend no issue slots and
+// no registers on staging.  Per plane, shared memory
+// holds on the tile plus an m-wide halo (periodic wrap in x, y):
+//   rho, m0, m1, m2, e, g22  (double-buffered plane buffers, filled by cp.async)
+//   g02 on the tile rows (x-halo), g12 on the tile columns (y-halo)  (same buffers)
+//   p, r = 1/rho  (formulas P:127; EOS P:259-266; computed once per point)
+// (g_i2 = D_z u_i come from the z-pass).  u_i = m_i r and T = gamma M^2 p r are
+// formed on the fly in register windows.  While plane z is computed, plane
+// z+1 streams into the other plane buffer (cp.async) and its low-storage
+// register W' (= A W + dt Rz from the z-pass) into L2, so HBM latency hides
+// behind the FP64 work.  Each thread evaluates derivatives from register windows of RX = RY = 4
+// consecutive outputs ((4 + 2m) shared loads for 4 outputs), and the 8 warps
+// split into a velocity group (A: velocity gradients, viscous Laplacians,
+// mixed derivatives, heat flux, dissipation) and a conservative group (B:
+// skew-symmetric advection and fluxes).
+//   phase X  : x-derivatives of tile rows (A, B) + g00, g10 on the halo rows (ext)
+//   phase Y  : y-derivatives (A, B), combined with phase-X partials
+//   epilogue : W <- W' + dt (A + B), Q' <- Q + B W  (low-storage RK)
+constexpr int XY_TX = 32;
+constexpr int XY_TY = 16;
+constexpr int XY_RX = 4;
+constexpr int XY_RY = 4;
+constexpr int XY_THREADS = 256;          // consumer threads
+#ifndef OSBLI_XY_PRODUCERS
+#define OSBLI_XY_PRODUCERS 4
+#endif
+constexpr int XY_PROD = 32 * OSBLI_XY_PRODUCERS;  // producer threads
+constexpr int XY_CTA = XY_THREADS + XY_PROD;
+// named barriers: 1 = consumers only; 2 + b = buffer b full; 4 + b = buffer b empty
+__device__ __forceinline__ void nbar_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void nbar_arrive(int id, int count) {
+  asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+#ifndef OSBLI_XY_SEG
+#define OSBLI_XY_SEG 8
+#endif
+constexpr int XY_SEG = OSBLI_XY_SEG;  // z-planes per CTA
+// full-halo fields of a plane buffer (S) and of the per-plane formula arrays (PR)
+enum { XF_RHO = 0, XF_M0, XF_M1, XF_M2, XF_E, XF_G22, XF_N };
+enum { XP_P = 0, XP_R = 1 };
+
+template <int M>
+struct XYGeom {
+  static constexpr int HX = XY_TX + 2 * M;
+  static constexpr int PX = HX | 1;         // odd pitch (doubles): conflict-free row-per-lane access
+  static constexpr int HY = XY_TY + 2 * M;
+  static constexpr int FSZ = HY * PX;       // one full-halo field
+  static constexpr int TP = XY_TX + 1;      // odd row pitch of tile-column arrays
+  static constexpr int NPT = TP * XY_TY;    // tile points (padded)
+  static constexpr int EXT = TP * HY;       // tile columns x (tile + y-halo) rows
+  static constexpr int W = 4 + 2 * M;       // window length (RX = RY = 4)
+  // plane buffer (doubles): 6 full-halo fields | g02 [TY][PX] (tile rows) | g12 [HY][TP] (tile cols)
+  static constexpr int PB_G02 = XF_N * FSZ;
+  static constexpr int PB_G12 = PB_G02 + XY_TY * PX;
+  static constexpr int PBSZ = PB_G12 + EXT;
+  // layout: PB[2] | PR (p, r) | E0 | E1 | XA[5] | XB[5]
+  static constexpr int OFF_PR = 2 * PBSZ;
+  static constexpr int OFF_E0 = OFF_PR + 2 * FSZ;   // [HY][TP]   g00 (y-extended)
+  static constexpr int OFF_E1 = OFF_E0 + EXT;       // [HY][TP]   g10 (y-extended)
+  static constexpr int OFF_XA = OFF_E1 + EXT;       // 5 x [TY][TP]
+  static constexpr int OFF_XB = OFF_XA + 5 * NPT;   // 5 x [TY][TP]
+  static constexpr int TOTAL = OFF_XB + 5 * NPT;
+  static constexpr int BYTES = TOTAL * (int)sizeof(double);
+};
+
+template <int M>
+constexpr int xy_smem_bytes() {
+  return XYGeom<M>::BYTES;
+}
+
+// Window elements that are products are rounded explicitly (__dmul_rn): the
+// compiler may otherwise contract a product into the stencil difference
+// (f+ - f-) differently for different taps, and a uniform state would no
+// longer cancel exactly (SURVEY §8(c) equilibrium pin).
+// window of W values starting at base, stride `st` (doubles)
+template <int W>
+__device__ __forceinline__ void ldwin(const double *base, int st, double (&v)[W]) {
+#pragma unroll
+  for (int k = 0; k < W; ++k) v[k] = base[k * st];
+}
+
+template <int M, int W>
+__device__ __forceinline__ double wd1(const KParams &p, const double (&v)[W], int j) {
+  // two interleaved partial sums halve the dependent FMA chain
+  double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+  for (int k = 1; k <= M; ++k) {
+    if (k & 1) s0 = fma(p.a[k - 1], v[j + M + k] - v[j + M - k], s0);
+    else s1 = fma(p.a[k - 1], v[j + M + k] - v[j + M - k], s1);
+  }
+  return s0 + s1;
+}
+
+// second derivative, exactly zero on a constant window: sum b_k ((f+ + f-) - 2 f)  (D-22)
+template <int M, int W>
+__device__ __forceinline__ double wd2(const KParams &p, const double (&v)[W], int j) {
+  const double c = v[j + M];
+  double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+  for (int k = 1; k <= M; ++k) {
+    const double t = fma(-2.0, c, v[j + M + k] + v[j + M - k]);
+    if (k & 1) s0 = fma(p.b[k], t, s0);
+    else s1 = fma(p.b[k], t, s1);
+  }
+  return s0 + s1;
+}
+
+// Velocity group, one direction (DIR 0 = x: phase X, DIR 1 = y: phase Y):
+// velocity gradients g_id, second derivatives of u_i and T along d, and the
+// mixed derivatives needed along d (commuted, D-7).
+template <int M>
+struct VelResult {
+  double g[3][4], d2u[3][4], d2T[4], mixA[4], mixB[4], mixC[4], mixD[4], uc[3][4];
+};
+
+template <int M, int DIR>
+__device__ __forceinline__ void velocity_dir(const KParams &p, const double *S, const double *PR,
+                                             int base, int st, const double *gmix, int gst,
+                                             const double *E0, const double *E1, int ebase,
+                                             VelResult<M> &o) {
+  using Gm = XYGeom<M>;
+  constexpr int W = Gm::W;
+  double r[W], v[W], t[W];
+  ldwin<W>(PR + XP_R * Gm::FSZ + base, st, r);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    ldwin<W>(S + (XF_M0 + i) * Gm::FSZ + base, st, t);
+#pragma unroll
+    for (int k = 0; k < W; ++k) v[k] = __dmul_rn(t[k], r[k]);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      o.g[i][j] = wd1<M, W>(p, v, j);
+      o.d2u[i][j] = wd2<M, W>(p, v, j);
+      o.uc[i][j] = v[j + M];
+    }
+  }
+  ldwin<W>(PR + XP_P * Gm::FSZ + base, st, t);
+#pragma unroll
+  for (int k = 0; k < W; ++k) v[k] = __dmul_rn(__dmul_rn(p.gM2, t[k]), r[k]);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) o.d2T[j] = wd2<M, W>(p, v, j);
+  ldwin<W>(S + XF_G22 * Gm::FSZ + base, st, v);  // D_d g22
+#pragma unroll
+  for (int j = 0; j < 4; ++j) o.mixA[j] = wd1<M, W>(p, v, j);
+  ldwin<W>(gmix, gst, v);  // DIR 0: D_x g02 = D_z g00 ; DIR 1: D_y g12 = D_z g11
+#pragma unroll
+  for (int j = 0; j < 4; ++j) o.mixB[j] = wd1<M, W>(p, v, j);
+  if (DIR == 1) {
+    ldwin<W>(E0 + ebase, Gm::TP, v);  // D_y g00
+#pragma unroll
+    for (int j = 0; j < 4; ++j) o.mixC[j] = wd1<M, W>(p, v, j);
+    ldwin<W>(E1 + ebase, Gm::TP, v);  // D_y g10 = D_x g11
+#pragma unroll
+    for (int j = 0; j < 4; ++j) o.mixD[j] = wd1<M, W>(p, v, j);
+  }
+}
+
+// Conservative group, one direction d: the d-part of
+//   -[ D_d F_id + 1/2 u_d D_d s ]  (and mass: -1/2 (D_d m_d + u_d D_d rho)),
+//   F_id = 1/2 m_i u_d + delta_id p,  G_d = (1/2 e + p) u_d   (skew halves + pressure)
+template <int M, int DIR>
+__device__ __forceinline__ void conservative_dir(const KParams &p, const double *S,
+                                                 const double *PR, int base, int st,
+                                                 double (&R)[5][4]) {
+  using Gm = XYGeom<M>;
+  constexpr int W = Gm::W;
+  double ud[W], pw[W], v[W], t[W];
+  {
+    double r[W];
+    ldwin<W>(PR + XP_R * Gm::FSZ + base, st, r);
+    ldwin<W>(S + (XF_M0 + DIR) * Gm::FSZ + base, st, t);
+#pragma unroll
+    for (int k = 0; k < W; ++k) ud[k] = __dmul_rn(t[k], r[k]);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) R[0][j] = -0.5 * wd1<M, W>(p, t, j);
+  }
+  ldwin<W>(S + XF_RHO * Gm::FSZ + base, st, v);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) R[0][j] = fma(-0.5 * ud[j + M], wd1<M, W>(p, v, j), R[0][j]);
+  ldwin<W>(PR + XP_P * Gm::FSZ + base, st, pw);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    ldwin<W>(S + (XF_M0 + i) * Gm::FSZ + base, st, v);
+#pragma unroll
+    for (int k = 0; k < W; ++k)
+      t[k] = (i == DIR) ? fma(0.5 * v[k], ud[k], pw[k]) : __dmul_rn(0.5 * v[k], ud[k]);
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      R[1 + i][j] = -fma(0.5 * ud[j + M], wd1<M, W>(p, v, j), wd1<M, W>(p, t, j));
+  }
+  ldwin<W>(S + XF_E * Gm::FSZ + base, st, v);
+#pragma unroll
+  for (int k = 0; k < W; ++k) t[k] = __dmul_rn(fma(0.5, v[k], pw[k]), ud[k]);
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    R[4][j] = -fma(0.5 * ud[j + M], wd1<M, W>(p, v, j), wd1<M, W>(p, t, j));
+}
+
+// issue the asynchronous copies of plane z's operands into plane buffer PB
+template <int M>
+__device__ __forceinline__ void xy_issue_plane(const KParams &p, const double *__restrict__ q,
+                                               const double *__restrict__ gz, double *PB, int z,
+                                               int x0, int y0, int tid, int nthr) {
+  using Gm = XYGeom<M>;
+  constexpr int HX = Gm::HX, HY = Gm::HY, PX = Gm::PX, FSZ = Gm::FSZ;
+  const size_t FS = (size_t)p.nx * p.ny;
+  const double *qp = q + qplane(p, z);
+  const double *gp = gz + (size_t)z * 3 * FS;
+  for (int idx = tid; idx < HY * HX; idx += nthr) {
+    const int hy = idx / HX, hx = idx - hy * HX;
+    const size_t off = (size_t)wrapi(y0 - M + hy, p.ny) * p.nx + wrapi(x0 - M + hx, p.nx);
+    double *d = PB + hy * PX + hx;
+#pragma unroll
+    for (int f = 0; f < 5; ++f) cp_async8(d + f * FSZ, qp + f * FS + off);
+    cp_async8(d + XF_G22 * FSZ, gp + 2 * FS + off);
+  }
+  for (int idx = tid; idx < XY_TY * HX; idx += nthr) {
+    const int ty = idx / HX, hx = idx - ty * HX;
+    const size_t off = (size_t)wrapi(y0 + ty, p.ny) * p.nx + wrapi(x0 - M + hx, p.nx);
+    cp_async8(PB + Gm::PB_G02 + ty * PX + hx, gp + off);
+  }
+  for (int idx = tid; idx < HY * XY_TX; idx += nthr) {
+    const int hy = idx >> 5, tx = idx & 31;
+    const size_t off = (size_t)wrapi(y0 - M + hy, p.ny) * p.nx + wrapi(x0 + tx, p.nx);
+    cp_async8(PB + Gm::PB_G12 + hy * Gm::TP + tx, gp + FS + off);
+  }
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+
+// L2 prefetch of plane z's epilogue operand W' on the tile rows
+__device__ __forceinline__ void xy_prefetch_epilogue(const KParams &p, const double *w, int z,
+                                                     int x0, int y0, int tid, int nthr) {
+  const size_t FS = (size_t)p.nx * p.ny;
+  for (int t = tid; t < XY_TY * 5 * 2; t += nthr) {
+    const int half = t & 1, a = (t >> 1) % 5, ty = (t >> 1) / 5;
+    const int y = y0 + ty, x = min(x0 + 16 * half, p.nx - 1);
+    if (y >= p.ny) continue;
+    asm volatile("prefetch.global.L2 [%0];\n" ::"l"(w + (size_t)z * 5 * FS + a * FS +
+                                                      (size_t)y * p.nx + x));
+  }
+}
+
+template <int M>
+__global__ void __launch_bounds__(XY_CTA, 1)
+    xypass_kernel(const KParams p, const double *__restrict__ q, double *__restrict__ qout,
+                  double *__restrict__ w, const double *__restrict__ gz,
+                  double *__restrict__ rout,
+                  unsigned int *__restrict__ flag, int z_begin, int z_end, int seg_len) {
+  using Gm = XYGeom<M>;
+  constexpr int HX = Gm::HX, HY = Gm::HY, PX = Gm::PX, FSZ = Gm::FSZ, NPT = Gm::NPT, TP = Gm::TP;
+  extern __shared__ double SM[];
+  double *PR = SM + Gm::OFF_PR;
+  double *E0 = SM + Gm::OFF_E0, *E1 = SM + Gm::OFF_E1;
+  double *XA = SM + Gm::OFF_XA, *XB = SM + Gm::OFF_XB;
+  const int tid = threadIdx.x;
+  const int x0 = blockIdx.x * XY_TX, y0 = blockIdx.y * XY_TY;
+  const int zs = z_begin + blockIdx.z * seg_len;
+  const int ze = min(z_end, zs + seg_len);
+  if (zs >= ze) return;
+  const size_t FS = (size_t)p.nx * p.ny;
+  const int grp = tid >> 7;  // 0: velocity group A, 1: conservative group B (warp-uniform)
+  const int q7 = tid & 127;
+  bool bad = false;
+
+  const int nplanes = ze - zs;
+  if (tid >= XY_THREADS) {
+    // ---- producer warpgroup: plane i into buffer i & 1 once the consumers released it;
+    //      it needs few registers and hands the rest to the consumer warpgroups
+#if OSBLI_XY_PRODUCERS == 4
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
+#endif
+    const int lane = tid - XY_THREADS;
+    for (int i = 0; i < nplanes; ++i) {
+      const int b = i & 1;
+      if (i >= 2) nbar_sync(4 + b, XY_CTA);
+      xy_issue_plane<M>(p, q, gz, SM + b * Gm::PBSZ, zs + i, x0, y0, lane, XY_PROD);
+      xy_prefetch_epilogue(p, w, zs + i, x0, y0, lane, XY_PROD);
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      nbar_arrive(2 + b, XY_CTA);
+    }
+    return;
+  }
+
+#if OSBLI_XY_PRODUCERS == 4
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
+#endif
+  for (int z = zs; z < ze; ++z) {
+    const int i = z - zs, cur = i & 1;
+    double *S = SM + cur * Gm::PBSZ;  // this plane's buffer
+    const double *G02 = S + Gm::PB_G02, *G12 = S + Gm::PB_G12;
+    // ---- plane z landed (producer): formulas p and 1/rho once per point
+    nbar_sync(2 + cur, XY_CTA);
+    for (int idx = tid; idx < HY * HX; idx += XY_THREADS) {
+      const int hy = idx / HX, hx = idx - hy * HX;
+      const int s = hy * PX + hx;
+      const double rho = S[XF_RHO * FSZ + s], m0 = S[XF_M0 * FSZ + s], m1 = S[XF_M1 * FSZ + s],
+                   m2 = S[XF_M2 * FSZ + s], e = S[XF_E * FSZ + s];
+      const double r = 1.0 / rho;
+      PR[XP_P * FSZ + s] = p.gm1 * (e - 0.5 * r * (m0 * m0 + m1 * m1 + m2 * m2));
+      PR[XP_R * FSZ + s] = r;
+    }
+    nbar_sync(1, XY_THREADS);
+
+    // ---- phase X: thread -> (row, 4-wide x segment); lanes 0-15 / 16-31 = 16 rows
+    {
+      const int row = q7 & 15, seg = q7 >> 4;
+      const int hy = row + M;
+      const int base = hy * PX + seg * XY_RX;  // window start (halo coords)
+      const int pt0 = row * TP + seg * XY_RX;
+      if (grp == 0) {
+        VelResult<M> o;
+        velocity_dir<M, 0>(p, S, PR, base, 1, G02 + row * PX + seg * XY_RX, 1, E0, E1, 0, o);
+        const double third = 1.0 / 3.0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          // x-parts of V_i: V0 += nu (4/3 D00 u0 + 1/3 D0 g22); V1 += nu D00 u1;
+          // V2 += nu (D00 u2 + 1/3 D0 g02)
+          const double V0 = p.nu * (o.d2u[0][j] + third * (o.d2u[0][j] + o.mixA[j]));
+          const double V1 = p.nu * o.d2u[1][j];
+          const double V2 = p.nu * (o.d2u[2][j] + third * o.mixB[j]);
+          XA[0 * NPT + pt0 + j] = V0;
+          XA[1 * NPT + pt0 + j] = V1;
+          XA[2 * NPT + pt0 + j] = V2;
+          XA[3 * NPT + pt0 + j] =
+              fma(p.kappa, o.d2T[j], o.uc[0][j] * V0 + o.uc[1][j] * V1 + o.uc[2][j] * V2);
+          XA[4 * NPT + pt0 + j] = o.g[2][j];          // g20
+          E0[hy * TP + seg * XY_RX + j] = o.g[0][j];  // g00
+          E1[hy * TP + seg * XY_RX + j] = o.g[1][j];  // g10
+        }
+      } else {
+        double R[5][4];
+        conservative_dir<M, 0>(p, S, PR, base, 1, R);
+#pragma unroll
+        for (int f = 0; f < 5; ++f)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) XB[f * NPT + pt0 + j] = R[f][j];
+      }
+    }
+    // ---- g00, g10 on the 2m halo rows (inner derivatives of D_y g00, D_y g10)
+    for (int task = tid; task < 2 * M * (XY_TX / XY_RX); task += XY_THREADS) {
+      const int rr = task % (2 * M), seg = task / (2 * M);
+      const int hy = rr < M ? rr : rr + XY_TY;
+      const int base = hy * PX + seg * XY_RX;
+      constexpr int W = Gm::W;
+      double r[W], v[W], t[W];
+      ldwin<W>(PR + XP_R * FSZ + base, 1, r);
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        ldwin<W>(S + (XF_M0 + i) * FSZ + base, 1, t);
+#pragma unroll
+        for (int k = 0; k < W; ++k) v[k] = __dmul_rn(t[k], r[k]);
+        double *Ei = i == 0 ? E0 : E1;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) Ei[hy * TP + seg * XY_RX + j] = wd1<M, W>(p, v, j);
+      }
+    }
+    nbar_sync(1, XY_THREADS);
+
+    // ---- phase Y: thread -> (column, 4-tall y segment); lanes = 32 consecutive columns
+    {
+      const int col = q7 & 31, seg = q7 >> 5;
+      const int base = (seg * XY_RY) * PX + col + M;
+      const int ebase = (seg * XY_RY) * TP + col;
+      if (grp == 0) {
+        VelResult<M> o;
+        velocity_dir<M, 1>(p, S, PR, base, PX, G12 + ebase, TP, E0, E1, ebase, o);
+        const double third = 1.0 / 3.0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int ty = seg * XY_RY + j;
+          const int pt = ty * TP + col;
+          const int c = (ty + M) * PX + col + M;
+          const double g00 = E0[(ty + M) * TP + col], g10 = E1[(ty + M) * TP + col];
+          const double g20 = XA[4 * NPT + pt];
+          const double g01 = o.g[0][j], g11 = o.g[1][j], g21 = o.g[2][j];
+          const double g02 = G02[ty * PX + col + M], g12 = G12[(ty + M) * TP + col],
+                       g22 = S[XF_G22 * FSZ + c];
+          // y-parts of V_i: V0 += nu (D11 u0 + 1/3 D1 g10);
+          // V1 += nu (4/3 D11 u1 + 1/3 (D1 g00 + D1 g22)); V2 += nu (D11 u2 + 1/3 D1 g12)
+          const double V0y = p.nu * (o.d2u[0][j] + third * o.mixD[j]);
+          const double V1y = p.nu * (o.d2u[1][j] + third * (o.d2u[1][j] + o.mixC[j] + o.mixA[j]));
+          const double V2y = p.nu * (o.d2u[2][j] + third * o.mixB[j]);
+          const double V0 = XA[0 * NPT + pt] + V0y, V1 = XA[1 * NPT + pt] + V1y,
+                       V2 = XA[2 * NPT + pt] + V2y;
+          const double thxy = g00 + g11, th = thxy + g22;
+          const double s01 = g01 + g10, s02 = g02 + g20, s12 = g12 + g21;
+          // tau_ij du_i/dx_j (eq. 8)
+          const double Phi = p.nu * (2.0 * (g00 * g00 + g11 * g11 + g22 * g22) + s01 * s01 +
+                                     s02 * s02 + s12 * s12 - (2.0 / 3.0) * th * th);
+          const double u0 = o.uc[0][j], u1 = o.uc[1][j], u2 = o.uc[2][j];
+          const double ex = XA[3 * NPT + pt];  // kappa D00 T + u_i V_i^x (phase X)
+          // dilatation halves of the skew terms, -1/2 s (g00 + g11)
+          XA[0 * NPT + pt] = -0.5 * S[XF_RHO * FSZ + c] * thxy;
+          XA[1 * NPT + pt] = fma(-0.5 * S[XF_M0 * FSZ + c], thxy, V0);
+          XA[2 * NPT + pt] = fma(-0.5 * S[XF_M1 * FSZ + c], thxy, V1);
+          XA[3 * NPT + pt] = fma(-0.5 * S[XF_M2 * FSZ + c], thxy, V2);
+          XA[4 * NPT + pt] = fma(-0.5 * S[XF_E * FSZ + c], thxy,
+                                 ex + fma(p.kappa, o.d2T[j], Phi) +
+                                     (u0 * V0y + u1 * V1y + u2 * V2y));
+        }
+      } else {
+        double R[5][4];
+        conservative_dir<M, 1>(p, S, PR, base, PX, R);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int pt = (seg * XY_RY + j) * TP + col;
+#pragma unroll
+          for (int f = 0; f < 5; ++f) XB[f * NPT + pt] += R[f][j];
+        }
+      }
+    }
+    nbar_sync(1, XY_THREADS);
+
+    // ---- epilogue: W <- W' + dt R_xy ; Q' <- Q + B W   (coalesced rows; residual mode:
+    //      dt = 1, A = 0 so that W' = Rz and R = W' + R_xy)
+    for (int lin = tid; lin < XY_TX * XY_TY; lin += XY_THREADS) {
+      const int ty = lin >> 5, tx = lin & 31;
+      const int pt = ty * TP + tx;
+      const int x = x0 + tx, y = y0 + ty;
+      if (x >= p.nx || y >= p.ny) continue;
+      const int c = (ty + M) * PX + tx + M;
+      const size_t o = (size_t)z * 5 * FS + (size_t)y * p.nx + x;
+      double *qo = qout ? qout + qplane(p, z) + (size_t)y * p.nx + x : nullptr;
+      double wp[5];
+#pragma unroll
+      for (int f = 0; f < 5; ++f) wp[f] = w[o + f * FS];
+      const int fidx[5] = {XF_RHO, XF_M0, XF_M1, XF_M2, XF_E};
+#pragma unroll
+      for (int f = 0; f < 5; ++f) {
+        const double wn = fma(p.dt, XA[f * NPT + pt] + XB[f * NPT + pt], wp[f]);
+        if (rout) {
+          rout[o + f * FS] = wn;
+          continue;
+        }
+        if (p.write_w) w[o + f * FS] = wn;
+        const double qn = fma(p.B, wn, S[fidx[f] * FSZ + c]);
+        qo[f * FS] = qn;
+        bad |= !isfinite(qn);
+      }
+    }
+    if (i + 2 < nplanes) nbar_arrive(4 + cur, XY_CTA);  // buffer free for plane i + 2
+  }
+  if (bad) atomicOr(flag, 1u);
+}
+
+}  // namespace ws

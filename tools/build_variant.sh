@@ -7,4 +7,4 @@ mkdir -p variants/$1
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC $2 \
   -c paper_1609_01277_b200/csrc/kernels.cu -o variants/$1/kernels.o
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o variants/lib_$1.so variants/$1/kernels.o \
-  paper_1609_01277_b200/csrc/api.o -L$NCCL_HOME/lib -l:libnccl.so.2 -Xlinker -rpath=$NCCL_HOME/lib -lcudart
+  paper_1609_01277_b200/csrc/api.o paper_1609_01277_b200/csrc/scalar.o paper_1609_01277_b200/csrc/scalar_api.o -L$NCCL_HOME/lib -l:libnccl.so.2 -Xlinker -rpath=$NCCL_HOME/lib -lcudart
