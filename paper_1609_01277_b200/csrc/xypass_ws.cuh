@@ -21,8 +21,9 @@ namespace ws {
 // mixed derivatives, heat flux, dissipation) and a conservative group (B:
 // skew-symmetric advection and fluxes).
 //   phase X  : x-derivatives of tile rows (A, B) + g00, g10 on the halo rows (ext)
-//   phase Y  : y-derivatives (A, B), combined with phase-X partials
-//   epilogue : W <- W' + dt (A + B), Q' <- Q + B W  (low-storage RK)
+//   phase Y  : y-derivatives (A, B), combined with phase-X partials; group B
+//              then completes the stage for its points:
+//              W <- W' + dt (A + B), Q' <- Q + B W  (low-storage RK)
 constexpr int XY_TX = 32;
 constexpr int XY_TY = 16;
 constexpr int XY_RX = 4;
@@ -33,7 +34,8 @@ constexpr int XY_THREADS = 256;          // consumer threads
 #endif
 constexpr int XY_PROD = 32 * OSBLI_XY_PRODUCERS;  // producer threads
 constexpr int XY_CTA = XY_THREADS + XY_PROD;
-// named barriers: 1 = consumers only; 2 + b = buffer b full; 4 + b = buffer b empty
+// named barriers: 1 = consumers only; 2 + b = buffer b full; 4 + b = buffer b empty;
+// 6 = group A -> group B hand-over at the end of phase Y
 __device__ __forceinline__ void nbar_sync(int id, int count) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
 }
@@ -407,47 +409,54 @@ __global__ void __launch_bounds__(XY_CTA, 1)
                                  ex + fma(p.kappa, o.d2T[j], Phi) +
                                      (u0 * V0y + u1 * V1y + u2 * V2y));
         }
+        // A's part of every point of this tile is final: hand over to group B
+        nbar_arrive(6, XY_THREADS);
+        if (i + 2 < nplanes) nbar_arrive(4 + cur, XY_CTA);  // done with this plane buffer
       } else {
-        double R[5][4];
-        conservative_dir<M, 1>(p, S, PR, base, PX, R);
+        // group B finishes the stage for its 4 points: W' (z-pass output) is loaded
+        // first so that its latency hides behind the y-derivatives
+        const int x = x0 + col;
+        const bool xin = x < p.nx;
+        double wp[5][4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const int pt = (seg * XY_RY + j) * TP + col;
+          const int y = min(y0 + seg * XY_RY + j, p.ny - 1);
+          const size_t o = (size_t)z * 5 * FS + (size_t)y * p.nx + (xin ? x : p.nx - 1);
 #pragma unroll
-          for (int f = 0; f < 5; ++f) XB[f * NPT + pt] += R[f][j];
+          for (int f = 0; f < 5; ++f) wp[f][j] = w[o + f * FS];
         }
+        double R[5][4];
+        conservative_dir<M, 1>(p, S, PR, base, PX, R);
+        nbar_sync(6, XY_THREADS);  // group A's parts are in XA
+        // ---- epilogue: W <- W' + dt R_xy ; Q' <- Q + B W  (rows of 32 columns; residual
+        //      mode: dt = 1, A = 0 so that W' = Rz and R = W' + R_xy)
+        const int fidx[5] = {XF_RHO, XF_M0, XF_M1, XF_M2, XF_E};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int ty = seg * XY_RY + j;
+          const int y = y0 + ty;
+          if (!xin || y >= p.ny) continue;
+          const int pt = ty * TP + col;
+          const int c = (ty + M) * PX + col + M;
+          const size_t o = (size_t)z * 5 * FS + (size_t)y * p.nx + x;
+          double *qo = qout ? qout + qplane(p, z) + (size_t)y * p.nx + x : nullptr;
+#pragma unroll
+          for (int f = 0; f < 5; ++f) {
+            const double rxy = XA[f * NPT + pt] + (XB[f * NPT + pt] + R[f][j]);
+            const double wn = fma(p.dt, rxy, wp[f][j]);
+            if (rout) {
+              rout[o + f * FS] = wn;
+              continue;
+            }
+            if (p.write_w) w[o + f * FS] = wn;
+            const double qn = fma(p.B, wn, S[fidx[f] * FSZ + c]);
+            qo[f * FS] = qn;
+            bad |= !isfinite(qn);
+          }
+        }
+        if (i + 2 < nplanes) nbar_arrive(4 + cur, XY_CTA);  // done with this plane buffer
       }
     }
-    nbar_sync(1, XY_THREADS);
-
-    // ---- epilogue: W <- W' + dt R_xy ; Q' <- Q + B W   (coalesced rows; residual mode:
-    //      dt = 1, A = 0 so that W' = Rz and R = W' + R_xy)
-    for (int lin = tid; lin < XY_TX * XY_TY; lin += XY_THREADS) {
-      const int ty = lin >> 5, tx = lin & 31;
-      const int pt = ty * TP + tx;
-      const int x = x0 + tx, y = y0 + ty;
-      if (x >= p.nx || y >= p.ny) continue;
-      const int c = (ty + M) * PX + tx + M;
-      const size_t o = (size_t)z * 5 * FS + (size_t)y * p.nx + x;
-      double *qo = qout ? qout + qplane(p, z) + (size_t)y * p.nx + x : nullptr;
-      double wp[5];
-#pragma unroll
-      for (int f = 0; f < 5; ++f) wp[f] = w[o + f * FS];
-      const int fidx[5] = {XF_RHO, XF_M0, XF_M1, XF_M2, XF_E};
-#pragma unroll
-      for (int f = 0; f < 5; ++f) {
-        const double wn = fma(p.dt, XA[f * NPT + pt] + XB[f * NPT + pt], wp[f]);
-        if (rout) {
-          rout[o + f * FS] = wn;
-          continue;
-        }
-        if (p.write_w) w[o + f * FS] = wn;
-        const double qn = fma(p.B, wn, S[fidx[f] * FSZ + c]);
-        qo[f * FS] = qn;
-        bad |= !isfinite(qn);
-      }
-    }
-    if (i + 2 < nplanes) nbar_arrive(4 + cur, XY_CTA);  // buffer free for plane i + 2
   }
   if (bad) atomicOr(flag, 1u);
 }
