@@ -35,7 +35,7 @@ class _CParams(ctypes.Structure):
     _fields_ = [("nx", ctypes.c_int), ("ny", ctypes.c_int), ("nz", ctypes.c_int),
                 ("order", ctypes.c_int), ("dx", ctypes.c_double), ("dt", ctypes.c_double),
                 ("Re", ctypes.c_double), ("Pr", ctypes.c_double), ("Minf", ctypes.c_double),
-                ("gamma", ctypes.c_double)]
+                ("gamma", ctypes.c_double), ("sym", ctypes.c_int * 3)]
 
 
 @dataclass
@@ -50,10 +50,11 @@ class OracleParams:
     Pr: float = 0.71
     Minf: float = 0.1
     gamma: float = 1.4
+    sym: tuple = (0, 0, 0)  # 1: symmetry boundaries in x, y, z; 0: periodic
 
     def c(self) -> _CParams:
         return _CParams(self.nx, self.ny, self.nz, self.order, self.dx, self.dt,
-                        self.Re, self.Pr, self.Minf, self.gamma)
+                        self.Re, self.Pr, self.Minf, self.gamma, (ctypes.c_int * 3)(*self.sym))
 
     @property
     def shape(self):

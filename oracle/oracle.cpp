@@ -146,11 +146,31 @@ bool central_weights(int order, std::vector<Frac>& a, std::vector<Frac>& b) {
 }
 
 // ---------------------------------------------------------------------------
-// Periodic grid: x_i = i*dx, i = 0..N-1, f[i+N] = f[i].
-// Arrays use the ABI layout [nz][ny][nx], x fastest.
+// Grid: x_i = i*dx, i = 0..N-1, arrays [nz][ny][nx], x fastest.
+// Boundaries per direction: periodic, f[i+N] = f[i]; or symmetry,
+// "phi(x_N) = phi(x_{N-1}) for scalar fields and phi_i(x_N) = -phi_i(x_{N-1})
+// for vector fields (in the direction i)": the halo mirrors the interior about
+// the boundary face (ghost -k <-> interior k-1, ghost N-1+k <-> interior N-k),
+// with the sign of the grid function's parity in that direction.
 // ---------------------------------------------------------------------------
+struct Par {  // parity of a grid function under the mirror of each direction
+  int s[3] = {1, 1, 1};
+};
+Par odd_in(int d) {
+  Par p;
+  p.s[d] = -1;
+  return p;
+}
+Par operator*(const Par& a, const Par& b) {
+  Par p;
+  for (int d = 0; d < 3; ++d) p.s[d] = a.s[d] * b.s[d];
+  return p;
+}
+const Par EVEN;
+
 struct Grid {
   int n[3];  // nx, ny, nz
+  int sym[3] = {0, 0, 0};  // 1: symmetry boundaries in that direction
   double dx;
   int m;
   std::vector<double> a;  // a_1..a_m  (first derivative)
@@ -159,32 +179,50 @@ struct Grid {
   size_t idx(int i, int j, int k) const {
     return ((size_t)k * n[1] + j) * n[0] + i;
   }
-  // index of the point displaced by s along direction dir (periodic wrap)
-  size_t shifted(int i, int j, int k, int dir, int s) const {
+  // index of the point displaced by s along direction dir; *flip = 1 when the
+  // value comes through an odd number of mirrors (symmetry boundaries)
+  size_t shifted(int i, int j, int k, int dir, int s, int* flip = nullptr) const {
     int c[3] = {i, j, k};
-    c[dir] = ((c[dir] + s) % n[dir] + n[dir]) % n[dir];
+    const int nd = n[dir];
+    int f = 0;
+    if (sym[dir]) {
+      int cm = ((c[dir] + s) % (2 * nd) + 2 * nd) % (2 * nd);
+      if (cm >= nd) {
+        cm = 2 * nd - 1 - cm;
+        f = 1;
+      }
+      c[dir] = cm;
+    } else {
+      c[dir] = ((c[dir] + s) % nd + nd) % nd;
+    }
+    if (flip) *flip = f;
     return idx(c[0], c[1], c[2]);
+  }
+  // value of grid function f (parity p) at the displaced point
+  double at(const double* f, const Par& p, int i, int j, int k, int dir, int s) const {
+    int fl = 0;
+    const double v = f[shifted(i, j, k, dir, s, &fl)];
+    return fl && p.s[dir] < 0 ? -v : v;
   }
 };
 
 // First derivative d f / d x_dir at (i,j,k):
 //   (1/dx) sum_{k=1..m} a_k (f[+k] - f[-k])
-double D1(const Grid& g, const double* f, int i, int j, int k, int dir) {
+double D1(const Grid& g, const double* f, int i, int j, int k, int dir, const Par& p = EVEN) {
   double s = 0.0;
   for (int t = 1; t <= g.m; ++t)
-    s += g.a[t - 1] * (f[g.shifted(i, j, k, dir, t)] - f[g.shifted(i, j, k, dir, -t)]);
+    s += g.a[t - 1] * (g.at(f, p, i, j, k, dir, t) - g.at(f, p, i, j, k, dir, -t));
   return s / g.dx;
 }
 
 // First derivative of the pointwise product f*h (the grid function f*h,
 // evaluated at each stencil point).
-double D1prod(const Grid& g, const double* f, const double* h, int i, int j, int k,
-              int dir) {
+double D1prod(const Grid& g, const double* f, const Par& pf, const double* h, const Par& ph,
+              int i, int j, int k, int dir) {
   double s = 0.0;
-  for (int t = 1; t <= g.m; ++t) {
-    const size_t ip = g.shifted(i, j, k, dir, t), im = g.shifted(i, j, k, dir, -t);
-    s += g.a[t - 1] * (f[ip] * h[ip] - f[im] * h[im]);
-  }
+  for (int t = 1; t <= g.m; ++t)
+    s += g.a[t - 1] * (g.at(f, pf, i, j, k, dir, t) * g.at(h, ph, i, j, k, dir, t) -
+                       g.at(f, pf, i, j, k, dir, -t) * g.at(h, ph, i, j, k, dir, -t));
   return s / g.dx;
 }
 
@@ -192,11 +230,11 @@ double D1prod(const Grid& g, const double* f, const double* h, int i, int j, int
 //   (1/dx^2) sum_{k=1..m} b_k ((f[+k] - f) + (f[-k] - f))
 // (equivalent to sum_{k=-m..m} w_k f[k] since b_0 = -2 sum b_k; this form is
 //  exactly zero on a constant field).
-double D2(const Grid& g, const double* f, int i, int j, int k, int dir) {
+double D2(const Grid& g, const double* f, int i, int j, int k, int dir, const Par& p = EVEN) {
   const double f0 = f[g.idx(i, j, k)];
   double s = 0.0;
   for (int t = 1; t <= g.m; ++t)
-    s += g.b[t] * ((f[g.shifted(i, j, k, dir, t)] - f0) + (f[g.shifted(i, j, k, dir, -t)] - f0));
+    s += g.b[t] * ((g.at(f, p, i, j, k, dir, t) - f0) + (g.at(f, p, i, j, k, dir, -t) - f0));
   return s / (g.dx * g.dx);
 }
 
@@ -242,7 +280,7 @@ void velocity_gradients(const Grid& G, Work& w) {
       for (int ix = 0; ix < G.n[0]; ++ix) {
         const size_t q = G.idx(ix, jy, k);
         for (int i = 0; i < 3; ++i)
-          for (int j = 0; j < 3; ++j) w.g[i][j][q] = D1(G, w.u[i].data(), ix, jy, k, j);
+          for (int j = 0; j < 3; ++j) w.g[i][j][q] = D1(G, w.u[i].data(), ix, jy, k, j, odd_in(i));
       }
 }
 
@@ -256,8 +294,14 @@ void residual(const Grid& G, const Phys& ph, const double* Q, double* R) {
   const double* rho = Q;
   const double* mom[3] = {Q + N, Q + 2 * N, Q + 3 * N};
   const double* e = Q + 4 * N;
-  // the conserved quantities rho*phi of the skew form: phi = 1, u_i, E
+  // the conserved quantities rho*phi of the skew form: phi = 1, u_i, E;
+  // parities under the mirrors: rho, E even; rho u_i odd in direction i
   const double* s_of[5] = {rho, mom[0], mom[1], mom[2], e};
+  const Par s_par[5] = {EVEN, odd_in(0), odd_in(1), odd_in(2), EVEN};
+  // g_ij = du_i/dx_j: parity of u_i times the flip of the derivative direction j
+  Par g_par[3][3];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) g_par[i][j] = odd_in(i) * odd_in(j);
   for (int k = 0; k < G.n[2]; ++k)
     for (int jy = 0; jy < G.n[1]; ++jy)
       for (int ix = 0; ix < G.n[0]; ++ix) {
@@ -275,8 +319,8 @@ void residual(const Grid& G, const Phys& ph, const double* Q, double* R) {
           const double* s = s_of[f];
           double c = 0.0;
           for (int j = 0; j < 3; ++j) {
-            const double flux = D1prod(G, s, w.u[j].data(), ix, jy, k, j);
-            const double adv = u[j] * D1(G, s, ix, jy, k, j);
+            const double flux = D1prod(G, s, s_par[f], w.u[j].data(), odd_in(j), ix, jy, k, j);
+            const double adv = u[j] * D1(G, s, ix, jy, k, j, s_par[f]);
             const double dil = s[q] * g[j][j];
             c += 0.5 * (flux + adv + dil);
           }
@@ -299,16 +343,16 @@ void residual(const Grid& G, const Phys& ph, const double* Q, double* R) {
         double V[3];
         for (int i = 0; i < 3; ++i) {
           double lap = 0.0;
-          for (int j = 0; j < 3; ++j) lap += D2(G, w.u[i].data(), ix, jy, k, j);
+          for (int j = 0; j < 3; ++j) lap += D2(G, w.u[i].data(), ix, jy, k, j, odd_in(i));
           double cross = 0.0;  // sum_j d/dx_j (du_j/dx_i)
           for (int j = 0; j < 3; ++j) {
-            if (j == i) cross += D2(G, w.u[i].data(), ix, jy, k, i);
-            else cross += D1(G, w.g[j][i].data(), ix, jy, k, j);
+            if (j == i) cross += D2(G, w.u[i].data(), ix, jy, k, i, odd_in(i));
+            else cross += D1(G, w.g[j][i].data(), ix, jy, k, j, g_par[j][i]);
           }
           double graddiv = 0.0;  // d/dx_i (du_k/dx_k)
           for (int kk = 0; kk < 3; ++kk) {
-            if (kk == i) graddiv += D2(G, w.u[i].data(), ix, jy, k, i);
-            else graddiv += D1(G, w.g[kk][kk].data(), ix, jy, k, i);
+            if (kk == i) graddiv += D2(G, w.u[i].data(), ix, jy, k, i, odd_in(i));
+            else graddiv += D1(G, w.g[kk][kk].data(), ix, jy, k, i, g_par[kk][kk]);
           }
           V[i] = nu * (lap + cross - 2.0 / 3.0 * graddiv);
         }
@@ -323,7 +367,7 @@ void residual(const Grid& G, const Phys& ph, const double* Q, double* R) {
         //     d/dx_j(u_i tau_ij) = tau_ij du_i/dx_j + u_i dtau_ij/dx_j (product rule, D-5)
         double pu = 0.0, heat = 0.0, work = 0.0, uv = 0.0;
         for (int j = 0; j < 3; ++j) {
-          pu += D1prod(G, w.p.data(), w.u[j].data(), ix, jy, k, j);
+          pu += D1prod(G, w.p.data(), EVEN, w.u[j].data(), odd_in(j), ix, jy, k, j);
           heat += D2(G, w.T.data(), ix, jy, k, j);
         }
         for (int i = 0; i < 3; ++i) {
@@ -404,6 +448,7 @@ extern "C" {
 struct oracle_params {
   int nx, ny, nz, order;
   double dx, dt, Re, Pr, Minf, gamma;
+  int sym[3];  // 1: symmetry boundaries in direction d, 0: periodic
 };
 
 static bool make_grid(const oracle_params* P, Grid& G) {
@@ -414,6 +459,7 @@ static bool make_grid(const oracle_params* P, Grid& G) {
   G.n[0] = P->nx;
   G.n[1] = P->ny;
   G.n[2] = P->nz;
+  for (int d = 0; d < 3; ++d) G.sym[d] = P->sym[d] ? 1 : 0;
   G.dx = P->dx;
   G.m = P->order / 2;
   G.a.clear();
@@ -533,7 +579,7 @@ static void scalar_residual(const Grid &G, const double u[3], double kd, const d
         const size_t q = G.idx(ix, jy, k);
         double adv = 0.0, lap = 0.0;
         for (int j = 0; j < 3; ++j) {
-          adv += D1prod(G, phi, uj[j].data(), ix, jy, k, j);
+          adv += D1prod(G, phi, EVEN, uj[j].data(), EVEN, ix, jy, k, j);
           lap += D2(G, phi, ix, jy, k, j);
         }
         R[q] = -adv + kd * lap - (S ? S[q] : 0.0);
