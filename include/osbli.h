@@ -47,6 +47,11 @@ extern "C" {
 
 typedef struct osbli_ctx osbli_ctx;
 
+/* Boundary conditions per direction: periodic (default), or symmetry at
+ * both ends of the direction: the halo mirrors the interior about the boundary
+ * face, scalars even, the momentum component normal to the face odd. */
+enum { OSBLI_BC_PERIODIC = 0, OSBLI_BC_SYMMETRY = 1 };
+
 /* Time schemes: forward Euler, and the 3-stage 2N-storage RK3
  * (Williamson coefficients in Carpenter-Kennedy 2N form; D-1). */
 enum { OSBLI_EULER = 0, OSBLI_RK3 = 1 };
@@ -135,6 +140,11 @@ int osbli_step(osbli_ctx *h, int n);
 /* Diagnostics of the current state (collective over ranks when distributed:
  * every rank gets the same, decomposition-independent numbers). */
 int osbli_diagnostics(osbli_ctx *h, osbli_diag *out);
+
+/* Boundary condition of direction dir (0 = x, 1 = y, 2 = z), both ends; takes
+ * effect at the next stage.  Symmetry in z is not built for slab-decomposed
+ * handles (OSBLI_E_UNSUPPORTED). */
+int osbli_set_boundary(osbli_ctx *h, int dir, int bc);
 
 /* Steady source term S added to the right-hand side, dQ/dt = R(Q) + S (the
  * method of manufactured solutions).  S is

@@ -9,6 +9,8 @@ PyTorch is used only for device memory and streams (torch tensors are passed
 as device pointers) and process groups (``init_distributed``).
 """
 from .native import (  # noqa: F401
+    OSBLI_BC_PERIODIC,
+    OSBLI_BC_SYMMETRY,
     OSBLI_EULER,
     OSBLI_RK3,
     LoopbackGroup,

@@ -557,6 +557,17 @@ int osbli_loopback_step(osbli_ctx **hs, int nslabs, int n) {
   return OSBLI_OK;
 }
 
+int osbli_set_boundary(osbli_ctx *h, int dir, int bc) {
+  int u = check_usable(h);
+  if (u) return u;
+  if (dir < 0 || dir > 2 || (bc != OSBLI_BC_PERIODIC && bc != OSBLI_BC_SYMMETRY))
+    return fail(h, OSBLI_E_INVAL, "bad direction or boundary type");
+  if (dir == 2 && bc == OSBLI_BC_SYMMETRY && h->nranks > 1)
+    return fail(h, OSBLI_E_UNSUPPORTED, "symmetry in z is not built for slab decompositions");
+  h->base.sym[dir] = bc;
+  return OSBLI_OK;
+}
+
 int osbli_set_source(osbli_ctx *h, const double *S, int on_device) {
   int u = check_usable(h);
   if (u) return u;

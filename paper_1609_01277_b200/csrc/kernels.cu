@@ -38,14 +38,35 @@ __device__ __forceinline__ int wrapi(int i, int n) {
   return i;
 }
 
+// boundary map of index i in a direction of n points: periodic wrap, or the
+// mirror about the boundary faces (symmetry: ghost -k <-> interior k-1,
+// ghost n-1+k <-> interior n-k); flip = 1 after an odd number of mirrors, where
+// a field's normal vector component changes sign
+__device__ __forceinline__ int bmap(int i, int n, int sym, int &flip) {
+  if (!sym) {
+    flip = 0;
+    return wrapi(i, n);
+  }
+  int c = i % (2 * n);
+  if (c < 0) c += 2 * n;
+  flip = c >= n;
+  return flip ? 2 * n - 1 - c : c;
+}
+
 __device__ __forceinline__ size_t qplane(const KParams &p, int z) {
   return (size_t)(z + p.G) * 5 * (size_t)p.nx * p.ny;
 }
 
-// z index of the plane read for logical plane z (wrap on one GPU, ghosts otherwise)
-__device__ __forceinline__ int zread(const KParams &p, int z) {
-  if (p.zwrap) return wrapi(z, p.nz);
+// z index of the plane read for logical plane z (wrap or mirror on one GPU,
+// ghost planes otherwise); flip = 1 when rho u_z changes sign (mirror)
+__device__ __forceinline__ int zread(const KParams &p, int z, int &flip) {
+  if (p.zwrap) return bmap(z, p.nz, p.sym[2], flip);
+  flip = 0;
   return max(-p.G, min(z, p.nz - 1 + p.G));
+}
+__device__ __forceinline__ int zread(const KParams &p, int z) {
+  int f;
+  return zread(p, z, f);
 }
 
 // 8-byte asynchronous global -> shared copy (LDGSTS); completed with cp.async.wait_group
@@ -93,16 +114,22 @@ __global__ void __launch_bounds__(256) diag_kernel(const KParams p, const double
       double sx = 0.0, sy = 0.0, sz = 0.0;
 #pragma unroll
       for (int k = 1; k <= M; ++k) {
-        const size_t rowp = (size_t)y * p.nx, zp_ = (size_t)(zread(p, z + k) + p.G) * 3 * FS,
-                     zm_ = (size_t)(zread(p, z - k) + p.G) * 3 * FS,
-                     z0_ = (size_t)(z + p.G) * 3 * FS;
+        // taps with the parity of u_i: odd under the mirror of direction i
+        int fxp, fxm, fyp, fym, fzp, fzm;
+        const int xp = bmap(x + k, p.nx, p.sym[0], fxp), xm = bmap(x - k, p.nx, p.sym[0], fxm);
+        const int yp = bmap(y + k, p.ny, p.sym[1], fyp), ym = bmap(y - k, p.ny, p.sym[1], fym);
+        const int zpl = zread(p, z + k, fzp), zml = zread(p, z - k, fzm);
+        const size_t rowp = (size_t)y * p.nx, zp_ = (size_t)(zpl + p.G) * 3 * FS,
+                     zm_ = (size_t)(zml + p.G) * 3 * FS, z0_ = (size_t)(z + p.G) * 3 * FS;
+        auto sg = [&](int fl, int d) { return (fl && i == d) ? -1.0 : 1.0; };
         sx = fma(p.a[k - 1],
-                 ui[z0_ + rowp + wrapi(x + k, p.nx)] - ui[z0_ + rowp + wrapi(x - k, p.nx)], sx);
+                 sg(fxp, 0) * ui[z0_ + rowp + xp] - sg(fxm, 0) * ui[z0_ + rowp + xm], sx);
         sy = fma(p.a[k - 1],
-                 ui[z0_ + (size_t)wrapi(y + k, p.ny) * p.nx + x] -
-                     ui[z0_ + (size_t)wrapi(y - k, p.ny) * p.nx + x],
+                 sg(fyp, 1) * ui[z0_ + (size_t)yp * p.nx + x] -
+                     sg(fym, 1) * ui[z0_ + (size_t)ym * p.nx + x],
                  sy);
-        sz = fma(p.a[k - 1], ui[zp_ + rowp + x] - ui[zm_ + rowp + x], sz);
+        sz = fma(p.a[k - 1], sg(fzp, 2) * ui[zp_ + rowp + x] - sg(fzm, 2) * ui[zm_ + rowp + x],
+                 sz);
       }
       g[i][0] = sx;
       g[i][1] = sy;

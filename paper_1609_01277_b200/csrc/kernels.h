@@ -22,6 +22,7 @@ struct KParams {
   double A, B, dt;
   int read_w, write_w;     // A != 0 ; W needed by a later stage
   const double *src;       // optional steady source S, [nz][5][ny][nx] (dQ/dt = R + S)
+  int sym[3];              // 1: symmetry boundaries in direction d, 0: periodic
 };
 
 // Device buffers of one handle.  Q buffers: [nz + 2G][5][ny][nx] (plane-major,

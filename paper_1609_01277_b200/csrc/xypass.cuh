@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(XY_THREADS, 1)
     S[XF_G22 * FSZ + s] = v[7];
   };
   bool paired = false;
-  if constexpr (M % 2 == 0) paired = (p.nx % 2 == 0);
+  if constexpr (M % 2 == 0) paired = (p.nx % 2 == 0) && !(p.sym[0] | p.sym[1]);
   if (paired) {
     // m and nx even: x0 - m + hx is even for even hx and never straddles the
     // periodic seam, so two neighbouring columns come in one 16-byte load
@@ -274,12 +274,17 @@ __global__ void __launch_bounds__(XY_THREADS, 1)
       const int idx = tid + it * XY_THREADS;
       if (idx < HX * HY) {
         const int hy = idx / HX, hx = idx - hy * HX;
-        const int x = wrapi(x0 - M + hx, p.nx), y = wrapi(y0 - M + hy, p.ny);
+        int fx, fy;
+        const int x = bmap(x0 - M + hx, p.nx, p.sym[0], fx),
+                  y = bmap(y0 - M + hy, p.ny, p.sym[1], fy);
         const size_t off = (size_t)y * p.nx + x;
 #pragma unroll
         for (int f = 0; f < 5; ++f) raw[it][f] = __ldg(qp + f * FS + off);
 #pragma unroll
         for (int f = 0; f < 3; ++f) raw[it][5 + f] = __ldg(gp + f * FS + off);
+        // symmetry boundaries: odd components under a mirror change sign
+        if (fx) { raw[it][1] = -raw[it][1]; raw[it][5] = -raw[it][5]; }
+        if (fy) { raw[it][2] = -raw[it][2]; raw[it][6] = -raw[it][6]; }
       }
     }
 #pragma unroll

@@ -219,7 +219,9 @@ __device__ __forceinline__ void xy_issue_plane(const KParams &p, const double *_
   const double *gp = gz + (size_t)z * 3 * FS;
   for (int idx = tid; idx < HY * HX; idx += nthr) {
     const int hy = idx / HX, hx = idx - hy * HX;
-    const size_t off = (size_t)wrapi(y0 - M + hy, p.ny) * p.nx + wrapi(x0 - M + hx, p.nx);
+    int fx, fy;
+    const size_t off = (size_t)bmap(y0 - M + hy, p.ny, p.sym[1], fy) * p.nx +
+                       bmap(x0 - M + hx, p.nx, p.sym[0], fx);
     double *d = PB + hy * PX + hx;
 #pragma unroll
     for (int f = 0; f < 5; ++f) cp_async8(d + f * FSZ, qp + f * FS + off);
@@ -227,15 +229,43 @@ __device__ __forceinline__ void xy_issue_plane(const KParams &p, const double *_
   }
   for (int idx = tid; idx < XY_TY * HX; idx += nthr) {
     const int ty = idx / HX, hx = idx - ty * HX;
-    const size_t off = (size_t)wrapi(y0 + ty, p.ny) * p.nx + wrapi(x0 - M + hx, p.nx);
+    int fx, fy;
+    const size_t off = (size_t)bmap(y0 + ty, p.ny, p.sym[1], fy) * p.nx +
+                       bmap(x0 - M + hx, p.nx, p.sym[0], fx);
     cp_async8(PB + Gm::PB_G02 + ty * PX + hx, gp + off);
   }
   for (int idx = tid; idx < HY * XY_TX; idx += nthr) {
     const int hy = idx >> 5, tx = idx & 31;
-    const size_t off = (size_t)wrapi(y0 - M + hy, p.ny) * p.nx + wrapi(x0 + tx, p.nx);
+    int fx, fy;
+    const size_t off = (size_t)bmap(y0 - M + hy, p.ny, p.sym[1], fy) * p.nx +
+                       bmap(x0 + tx, p.nx, p.sym[0], fx);
     cp_async8(PB + Gm::PB_G12 + hy * Gm::TP + tx, gp + FS + off);
   }
   asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+
+// Symmetry boundaries: the copies above fetched the mirrored interior
+// values; the components that are odd under a mirror change sign here
+// (rho u_x and g02 = D_z u_x under an x mirror, rho u_y and g12 under a y mirror).
+template <int M>
+__device__ __forceinline__ void xy_mirror_signs(const KParams &p, double *PB, int x0, int y0,
+                                                int tid, int nthr) {
+  using Gm = XYGeom<M>;
+  constexpr int HX = Gm::HX, HY = Gm::HY, PX = Gm::PX, FSZ = Gm::FSZ;
+  const bool xs = p.sym[0] && (x0 - M < 0 || x0 + XY_TX + M > p.nx);
+  const bool ys = p.sym[1] && (y0 - M < 0 || y0 + XY_TY + M > p.ny);
+  if (!xs && !ys) return;
+  for (int idx = tid; idx < HY * HX; idx += nthr) {
+    const int hy = idx / HX, hx = idx - hy * HX;
+    int fx, fy;
+    bmap(x0 - M + hx, p.nx, p.sym[0], fx);
+    bmap(y0 - M + hy, p.ny, p.sym[1], fy);
+    double *d = PB + hy * PX + hx;
+    if (fx) d[XF_M0 * FSZ] = -d[XF_M0 * FSZ];
+    if (fy) d[XF_M1 * FSZ] = -d[XF_M1 * FSZ];
+    if (fx && hy >= M && hy < M + XY_TY) PB[Gm::PB_G02 + (hy - M) * PX + hx] *= -1.0;
+    if (fy && hx >= M && hx < M + XY_TX) PB[Gm::PB_G12 + hy * Gm::TP + hx - M] *= -1.0;
+  }
 }
 
 // L2 prefetch of plane z's epilogue operand W' on the tile rows
@@ -287,6 +317,10 @@ __global__ void __launch_bounds__(XY_CTA, 1)
       xy_issue_plane<M>(p, q, gz, SM + b * Gm::PBSZ, zs + i, x0, y0, lane, XY_PROD);
       xy_prefetch_epilogue(p, w, zs + i, x0, y0, lane, XY_PROD);
       asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      if (p.sym[0] | p.sym[1]) {
+        nbar_sync(7, XY_PROD);  // every producer's copies have landed
+        xy_mirror_signs<M>(p, SM + b * Gm::PBSZ, x0, y0, lane, XY_PROD);
+      }
       nbar_arrive(2 + b, XY_CTA);
     }
     return;

@@ -132,9 +132,11 @@ __global__ void __launch_bounds__(ZP_THREADS, 1)
       const int idx = tid + it * ZP_THREADS;
       if (idx < NR * 32) {
         const int pl = idx >> 5;
-        const double *qp = q + qplane(p, zread(p, zs - M + pl)) + rowoff;
+        int fl;
+        const double *qp = q + qplane(p, zread(p, zs - M + pl, fl)) + rowoff;
 #pragma unroll
         for (int f = 0; f < 5; ++f) raw[it][f] = __ldg(qp + f * FS);
+        if (fl) raw[it][3] = -raw[it][3];  // rho u_z is odd under a z mirror
       }
     }
 #pragma unroll
@@ -247,9 +249,12 @@ __global__ void __launch_bounds__(ZP_THREADS, 1)
       for (int idx = tid; idx < ZP_TZ * 32; idx += ZP_THREADS) {
         const int j = idx >> 5;
         const int slot = ((k + 1) * ZP_TZ + 2 * M + j) % NR;
+        int fl;
+        zread(p, zs + (k + 1) * ZP_TZ + M + j, fl);
+        const double m2 = RB[(3 * ZP_TZ + j) * 32 + lane];
         zstore<M>(p, S, slot, lane, RB[(0 * ZP_TZ + j) * 32 + lane],
                   RB[(1 * ZP_TZ + j) * 32 + lane], RB[(2 * ZP_TZ + j) * 32 + lane],
-                  RB[(3 * ZP_TZ + j) * 32 + lane], RB[(4 * ZP_TZ + j) * 32 + lane]);
+                  fl ? -m2 : m2, RB[(4 * ZP_TZ + j) * 32 + lane]);
       }
       __syncthreads();  // ring updated, staging buffer free
       if (k + 2 < nchunks) issue_raw(k + 2);

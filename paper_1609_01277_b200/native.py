@@ -17,6 +17,8 @@ _lib = None
 
 OSBLI_EULER = 0
 OSBLI_RK3 = 1
+OSBLI_BC_PERIODIC = 0
+OSBLI_BC_SYMMETRY = 1
 _STATUS = {0: "OK", -1: "E_INVAL", -2: "E_UNSUPPORTED", -3: "E_NOMEM", -4: "E_CUDA",
            -5: "E_COMM", -6: "E_NONFINITE", -7: "E_STATE"}
 
@@ -80,6 +82,7 @@ def load():
                                         ctypes.POINTER(H)]
     L.osbli_loopback_step.argtypes = [ctypes.POINTER(H), c_int, c_int]
     L.osbli_set_source.argtypes = [H, vp, c_int]
+    L.osbli_set_boundary.argtypes = [H, c_int, c_int]
     L.osbli_scalar_create.argtypes = [c_int, c_int, c_int, c_int, c_double, c_double, c_double,
                                       c_double, c_double, c_double, c_int, ctypes.POINTER(H)]
     for fn in ("osbli_scalar_set_state", "osbli_scalar_set_source", "osbli_scalar_get_state",
@@ -216,6 +219,10 @@ class Solver:
 
     def sync(self):
         self._check(self._L.osbli_sync(self._h))
+
+    def set_boundary(self, direction: int, bc: int):
+        """OSBLI_BC_PERIODIC or OSBLI_BC_SYMMETRY for direction 0/1/2."""
+        self._check(self._L.osbli_set_boundary(self._h, int(direction), int(bc)))
 
     def set_source(self, S):
         """Steady source: dQ/dt = R(Q) + S (None removes it)."""
