@@ -116,7 +116,8 @@ def residual(p: OracleParams, Q: np.ndarray) -> np.ndarray:
 
 
 def step(p: OracleParams, Q: np.ndarray, scheme: int, nsteps: int) -> np.ndarray:
-    """Return Q advanced by nsteps (scheme 0 = Euler, 1 = RK3); input untouched."""
+    """Return Q advanced by nsteps (scheme 0 = Euler, 1 = RK3 2N, 2 = RK3 two-register);
+    input untouched."""
     Qn = np.array(Q, dtype=np.float64, order="C").reshape(p.shape).copy()
     if _L().oracle_step(ctypes.byref(p.c()), _dp(Qn), scheme, nsteps):
         raise ValueError("bad step arguments")
@@ -157,7 +158,7 @@ def scalar_residual(p: OracleParams, u, k: float, phi: np.ndarray, S=None) -> np
 
 
 def scalar_step(p: OracleParams, u, k: float, phi: np.ndarray, scheme: int, nsteps: int, S=None):
-    """phi advanced by nsteps (0 = Euler, 1 = RK3); input untouched."""
+    """phi advanced by nsteps (0 = Euler, 1 = RK3 2N, 2 = RK3 two-register); input untouched."""
     ph = np.array(phi, dtype=np.float64, order="C").reshape(p.nz, p.ny, p.nx).copy()
     Sc = None if S is None else np.ascontiguousarray(S, dtype=np.float64).reshape(ph.shape)
     Sp = None if Sc is None else _dp(Sc)

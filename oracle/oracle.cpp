@@ -437,6 +437,11 @@ void diagnostics(const Grid& G, const Phys& ph, const double* Q, double out[3]) 
 //   per stage s: W <- A_s W + dt R(Q);  Q <- Q + B_s W
 const double RK_A[3] = {0.0, -5.0 / 9.0, -153.0 / 128.0};
 const double RK_B[3] = {1.0 / 3.0, 15.0 / 16.0, 8.0 / 15.0};
+// The two-register ("SBLI") form of a third-order RK (SURVEY §8(c) row 1, §8(f)
+// N2; D-25), per stage s, with Q_old = Q at the start of the step:
+//   R = R(Q);  Q <- Q_old + alpha_s dt R;  Q_old <- Q_old + beta_s dt R
+const double RK2R_ALPHA[3] = {2.0 / 3.0, 5.0 / 12.0, 3.0 / 5.0};
+const double RK2R_BETA[3] = {1.0 / 4.0, 3.0 / 20.0, 3.0 / 5.0};
 
 }  // namespace
 
@@ -516,10 +521,11 @@ int oracle_residual(const oracle_params* P, const double* Q, double* R) {
   return 0;
 }
 
-// scheme 0 = forward Euler, 1 = RK3 (2N).  Q is advanced in place by nsteps.
+// scheme 0 = forward Euler, 1 = RK3 (2N), 2 = RK3 (two-register form).
+// Q is advanced in place by nsteps.
 int oracle_step(const oracle_params* P, double* Q, int scheme, int nsteps) {
   Grid G;
-  if (!make_grid(P, G) || (scheme != 0 && scheme != 1) || nsteps < 0) return -1;
+  if (!make_grid(P, G) || scheme < 0 || scheme > 2 || nsteps < 0) return -1;
   Phys ph{P->Re, P->Pr, P->Minf, P->gamma};
   const size_t n5 = 5 * G.npts();
   std::vector<double> R(n5), W(n5, 0.0);
@@ -527,6 +533,15 @@ int oracle_step(const oracle_params* P, double* Q, int scheme, int nsteps) {
     if (scheme == 0) {
       residual(G, ph, Q, R.data());
       for (size_t q = 0; q < n5; ++q) Q[q] = Q[q] + P->dt * R[q];
+    } else if (scheme == 2) {
+      std::vector<double> Qold(Q, Q + n5);
+      for (int s = 0; s < 3; ++s) {
+        residual(G, ph, Q, R.data());
+        for (size_t q = 0; q < n5; ++q) {
+          Q[q] = Qold[q] + RK2R_ALPHA[s] * (P->dt * R[q]);
+          Qold[q] = Qold[q] + RK2R_BETA[s] * (P->dt * R[q]);
+        }
+      }
     } else {
       for (int s = 0; s < 3; ++s) {
         // periodic halos are refreshed before every stage (D-10): the
@@ -594,17 +609,27 @@ int oracle_scalar_residual(const oracle_params *P, const double *u3, double kd, 
   return 0;
 }
 
-// scheme 0 = forward Euler, 1 = RK3 (2N, D-1); phi advanced in place.
+// scheme 0 = forward Euler, 1 = RK3 (2N, D-1), 2 = RK3 (two-register form, D-25);
+// phi advanced in place.
 int oracle_scalar_step(const oracle_params *P, const double *u3, double kd, const double *S,
                        double *phi, int scheme, int nsteps) {
   Grid G;
-  if (!make_grid(P, G) || !u3 || !phi || (scheme != 0 && scheme != 1) || nsteps < 0) return -1;
+  if (!make_grid(P, G) || !u3 || !phi || scheme < 0 || scheme > 2 || nsteps < 0) return -1;
   const size_t N = G.npts();
   std::vector<double> R(N), W(N, 0.0);
   for (int it = 0; it < nsteps; ++it) {
     if (scheme == 0) {
       scalar_residual(G, u3, kd, phi, S, R.data());
       for (size_t q = 0; q < N; ++q) phi[q] = phi[q] + P->dt * R[q];
+    } else if (scheme == 2) {
+      std::vector<double> old(phi, phi + N);
+      for (int s = 0; s < 3; ++s) {
+        scalar_residual(G, u3, kd, phi, S, R.data());
+        for (size_t q = 0; q < N; ++q) {
+          phi[q] = old[q] + RK2R_ALPHA[s] * (P->dt * R[q]);
+          old[q] = old[q] + RK2R_BETA[s] * (P->dt * R[q]);
+        }
+      }
     } else {
       for (int s = 0; s < 3; ++s) {
         scalar_residual(G, u3, kd, phi, S, R.data());

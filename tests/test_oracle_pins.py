@@ -186,7 +186,7 @@ def test_mms_inviscid_matches_jets_too(oracle_lib):
 
 
 # --------------------------------------------------------------------------- time stepping
-@pytest.mark.parametrize("scheme", [0, 1])
+@pytest.mark.parametrize("scheme", [0, 1, 2])
 @pytest.mark.parametrize("order", [4, 8])
 def test_entropy_wave_amplification_closed_form(oracle_lib, scheme, order):
     """Inviscid entropy wave rho = 1 + A sin(kx), u = U, p = p0 stays on the linear
@@ -230,7 +230,7 @@ def test_paper_wave_error_magnitude(oracle_lib):
     assert 0.1 * g["error_order_of_magnitude"] < err < 10 * g["error_order_of_magnitude"], err
 
 
-@pytest.mark.parametrize("scheme,expected", [(0, 1.0), (1, 3.0)])
+@pytest.mark.parametrize("scheme,expected", [(0, 1.0), (1, 3.0), (2, 3.0)])
 def test_temporal_order_nonlinear(oracle_lib, scheme, expected):
     """Observed temporal order on the nonlinear NS: refine dt at
     fixed grid against a much finer dt.  Pins the RK3 tableau as third order for
@@ -240,7 +240,7 @@ def test_temporal_order_nonlinear(oracle_lib, scheme, expected):
     n = 8
     dx = 2 * math.pi / n
     Q0 = perturbed_tgv(n, n, n, dx=dx, amp=0.05, kmax=2)
-    if scheme == 1:
+    if scheme in (1, 2):
         phys, T, dts, ref_dt = TGV_PHYS, 0.4, [0.04, 0.02, 0.01], 0.0025
     else:
         phys = dict(TGV_PHYS, Minf=0.5)
@@ -253,6 +253,39 @@ def test_temporal_order_nonlinear(oracle_lib, scheme, expected):
     e = [np.abs(sols[dt] - sols[ref_dt]).max() for dt in dts]
     slope = math.log(e[1] / e[2]) / math.log(2)
     assert abs(slope - expected) < 0.15, (e, slope)
+
+
+def test_two_register_rk3_is_its_butcher_tableau(oracle_lib):
+    """N2 (D-25): the two-register form Q <- Q_old + alpha_s dt R, Q_old += beta_s dt R
+    with alpha = (2/3, 5/12, 3/5), beta = (1/4, 3/20, 3/5) is the explicit RK with
+    c = (0, 2/3, 2/3), a21 = 2/3, a31 = 1/4, a32 = 5/12, b = (1/4, 3/20, 3/5).
+    The tableau satisfies the four third-order conditions exactly (rational
+    arithmetic), and one oracle step equals the stage-by-stage Butcher evaluation
+    (k_i = R(Q0 + dt sum_j a_ij k_j)) built from oracle residual calls: this
+    catches register mix-ups (updating Q_old before Q, alpha/beta swapped, a
+    stage reading Q_old) that the order tests alone might not."""
+    F = Fraction
+    a21, a31, a32 = F(2, 3), F(1, 4), F(5, 12)
+    b = (F(1, 4), F(3, 20), F(3, 5))
+    c = (F(0), a21, a31 + a32)
+    assert sum(b) == 1
+    assert sum(bi * ci for bi, ci in zip(b, c)) == F(1, 2)
+    assert sum(bi * ci * ci for bi, ci in zip(b, c)) == F(1, 3)
+    assert b[2] * a32 * c[1] == F(1, 6)
+    n = (10, 9, 8)
+    dx, dt = 0.4, 0.02
+    Q0 = perturbed_tgv(*n, dx=dx, amp=0.05, kmax=2)
+    p = oracle_lib.OracleParams(*n, 6, dx, dt=dt, **TGV_PHYS)
+    k1 = oracle_lib.residual(p, Q0)
+    k2 = oracle_lib.residual(p, Q0 + dt * float(a21) * k1)
+    k3 = oracle_lib.residual(p, Q0 + dt * (float(a31) * k1 + float(a32) * k2))
+    Q1 = Q0 + dt * (float(b[0]) * k1 + float(b[1]) * k2 + float(b[2]) * k3)
+    got = oracle_lib.step(p, Q0, 2, 1)
+    scale = np.abs(Q0.reshape(5, -1)).max(axis=1)
+    assert np.all(np.abs((got - Q1).reshape(5, -1)).max(axis=1) / scale < 1e-13)
+    # and it is a different third-order scheme from the 2N one (nonlinear problem)
+    other = oracle_lib.step(p, Q0, 1, 1)
+    assert np.abs(got - other).max() > 1e3 * np.abs(got - Q1).max()
 
 
 def test_euler_single_step_definition(oracle_lib):

@@ -37,7 +37,7 @@ def lam_h(order, kvec, u, kd, dx):
     return s
 
 
-@pytest.mark.parametrize("scheme", [0, 1])
+@pytest.mark.parametrize("scheme", [0, 1, 2])
 @pytest.mark.parametrize("direction", [0, 1, 2])
 def test_scalar_amplification_closed_form(oracle_lib, scheme, direction):
     """phi = sin(k x_d + 0.3): phi_n = Im(P(z)^n e^{i(k x_d + 0.3)}), z = dt lambda_h(k)."""
