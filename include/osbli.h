@@ -52,9 +52,12 @@ typedef struct osbli_ctx osbli_ctx;
  * face, scalars even, the momentum component normal to the face odd. */
 enum { OSBLI_BC_PERIODIC = 0, OSBLI_BC_SYMMETRY = 1 };
 
-/* Time schemes: forward Euler, and the 3-stage 2N-storage RK3
- * (Williamson coefficients in Carpenter-Kennedy 2N form; D-1). */
-enum { OSBLI_EULER = 0, OSBLI_RK3 = 1 };
+/* Time schemes: forward Euler, the 3-stage 2N-storage RK3
+ * (Williamson coefficients in Carpenter-Kennedy 2N form; D-1), and
+ * the two-register ("SBLI") third-order RK: per stage Q <- Q_old + alpha_s dt R,
+ * Q_old <- Q_old + beta_s dt R, alpha = (2/3, 5/12, 3/5), beta = (1/4, 3/20, 3/5)
+ * (D-25).  Same storage and traffic as OSBLI_RK3. */
+enum { OSBLI_EULER = 0, OSBLI_RK3 = 1, OSBLI_RK3_2R = 2 };
 
 enum {
   OSBLI_OK = 0,
@@ -81,7 +84,7 @@ typedef struct {
  *   nx,ny,nz >= 1 grid points; order even, 2..12 (else INVAL / UNSUPPORTED);
  *   dx > 0 isotropic spacing; dt > 0 time step;
  *   Re > 0 (Re = +INFINITY means inviscid: nu = kappa = 0); Pr > 0; Minf > 0;
- *   gamma > 1; scheme OSBLI_EULER or OSBLI_RK3.
+ *   gamma > 1; scheme OSBLI_EULER, OSBLI_RK3 or OSBLI_RK3_2R.
  * The state is zero until osbli_set_state.  *out receives the handle. */
 int osbli_create(int nx, int ny, int nz, int order, double dx, double dt, double Re, double Pr,
                  double Minf, double gamma, int scheme, osbli_ctx **out);

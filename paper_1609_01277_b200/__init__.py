@@ -13,6 +13,7 @@ from .native import (  # noqa: F401
     OSBLI_BC_SYMMETRY,
     OSBLI_EULER,
     OSBLI_RK3,
+    OSBLI_RK3_2R,
     LoopbackGroup,
     OsbliError,
     ScalarSolver,

@@ -98,7 +98,10 @@ int validate(int nx, int ny, int nz, int order, double dx, double dt, double Re,
   if (!(Pr > 0.0) || !std::isfinite(Pr)) { msg = "Pr must be > 0"; return OSBLI_E_INVAL; }
   if (!(Minf > 0.0) || !std::isfinite(Minf)) { msg = "Minf must be > 0"; return OSBLI_E_INVAL; }
   if (!(gamma > 1.0) || !std::isfinite(gamma)) { msg = "gamma must be > 1"; return OSBLI_E_INVAL; }
-  if (scheme != OSBLI_EULER && scheme != OSBLI_RK3) { msg = "scheme must be 0 or 1"; return OSBLI_E_INVAL; }
+  if (scheme != OSBLI_EULER && scheme != OSBLI_RK3 && scheme != OSBLI_RK3_2R) {
+    msg = "scheme must be 0, 1 or 2";
+    return OSBLI_E_INVAL;
+  }
   if (order > 2 * osbli::kMaxHalf) { msg = "orders above 12 are not built"; return OSBLI_E_UNSUPPORTED; }
   return OSBLI_OK;
 }
@@ -388,19 +391,33 @@ namespace {
 int run_stage(osbli_ctx *h, int s, bool exchange = true) {
   static const double RK_A[3] = {0.0, -5.0 / 9.0, -153.0 / 128.0};
   static const double RK_B[3] = {1.0 / 3.0, 15.0 / 16.0, 8.0 / 15.0};
+  static const double RK2R_ALPHA[3] = {2.0 / 3.0, 5.0 / 12.0, 3.0 / 5.0};
+  static const double RK2R_BETA[3] = {1.0 / 4.0, 3.0 / 20.0, 3.0 / 5.0};
   KParams p = h->base;
+  double *qin = h->b.q[h->cur], *qout = h->b.q[h->cur ^ 1];
+  double *wz = h->b.w;  // z-pass output W'
   if (h->scheme == OSBLI_RK3) {
     p.A = RK_A[s];
     p.B = RK_B[s];
     p.read_w = (s > 0);
     p.write_w = (s < 2);
+  } else if (h->scheme == OSBLI_RK3_2R) {
+    // Q' = Q_old + alpha_s dt R ; Q_old += beta_s dt R (D-25).  The z-pass part
+    // dt Rz goes to the interior planes of the destination buffer, which the
+    // xy-pass then overwrites point by point with Q'.
+    p.A = 0.0;
+    p.B = RK2R_ALPHA[s];
+    p.beta = RK2R_BETA[s];
+    p.two_reg = 1;
+    p.read_w = (s > 0);
+    p.write_w = (s < 2);
+    wz = qout + (size_t)h->base.G * 5 * ((size_t)h->nx * h->ny);
   } else {
     p.A = 0.0;
     p.B = 1.0;
     p.read_w = 0;
     p.write_w = 0;
   }
-  double *qin = h->b.q[h->cur], *qout = h->b.q[h->cur ^ 1];
   cudaEvent_t *ev = nullptr;
   if (h->timing) {
     if (h->ev_used + 3 > h->events.size()) {
@@ -415,7 +432,7 @@ int run_stage(osbli_ctx *h, int s, bool exchange = true) {
   }
   if (h->nranks == 1) {
     if (ev) CK(h, cudaEventRecord(ev[0], h->stream));
-    CK(h, osbli::launch_zpass(p, qin, h->b.w, h->b.gz, 0, h->nz, h->stream, &h->launches));
+    CK(h, osbli::launch_zpass(p, qin, wz, h->b.gz, 0, h->nz, h->stream, &h->launches));
     if (ev) CK(h, cudaEventRecord(ev[1], h->stream));
     CK(h, osbli::launch_xypass(p, qin, qout, h->b.w, h->b.gz, nullptr, h->b.flag, 0, h->nz,
                                h->stream, &h->launches));
@@ -441,10 +458,10 @@ int run_stage(osbli_ctx *h, int s, bool exchange = true) {
     if (r) return r;
   }
   if (ev) CK(h, cudaEventRecord(ev[0], h->stream));
-  CK(h, osbli::launch_zpass(p, qin, h->b.w, h->b.gz, lo, hi, h->stream, &h->launches));
+  CK(h, osbli::launch_zpass(p, qin, wz, h->b.gz, lo, hi, h->stream, &h->launches));
   if (h->comm) CK(h, cudaStreamWaitEvent(h->stream, h->ev_ghost, 0));
-  CK(h, osbli::launch_zpass(p, qin, h->b.w, h->b.gz, 0, lo, h->stream, &h->launches));
-  CK(h, osbli::launch_zpass(p, qin, h->b.w, h->b.gz, hi, h->nz, h->stream, &h->launches));
+  CK(h, osbli::launch_zpass(p, qin, wz, h->b.gz, 0, lo, h->stream, &h->launches));
+  CK(h, osbli::launch_zpass(p, qin, wz, h->b.gz, hi, h->nz, h->stream, &h->launches));
   if (ev) CK(h, cudaEventRecord(ev[1], h->stream));
   CK(h, osbli::launch_xypass(p, qin, qout, h->b.w, h->b.gz, nullptr, h->b.flag, 0, lo, h->stream,
                              &h->launches));
@@ -458,7 +475,7 @@ int run_stage(osbli_ctx *h, int s, bool exchange = true) {
   return OSBLI_OK;
 }
 
-int nstages(const osbli_ctx *h) { return h->scheme == OSBLI_RK3 ? 3 : 1; }
+int nstages(const osbli_ctx *h) { return h->scheme == OSBLI_EULER ? 1 : 3; }
 
 }  // namespace
 

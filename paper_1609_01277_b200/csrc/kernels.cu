@@ -68,6 +68,21 @@ __device__ __forceinline__ int zread(const KParams &p, int z) {
   int f;
   return zread(p, z, f);
 }
+// compile-time variant of bmap: SYM = false is the plain periodic wrap
+template <bool SYM>
+__device__ __forceinline__ int bmap_t(int i, int n, int sym, int &flip) {
+  if (SYM) return bmap(i, n, sym, flip);
+  flip = 0;
+  return wrapi(i, n);
+}
+// compile-time variant: SYM = false is the periodic / ghost-plane read (flip = 0)
+template <bool SYM>
+__device__ __forceinline__ int zread_t(const KParams &p, int z, int &flip) {
+  if (SYM) return zread(p, z, flip);
+  flip = 0;
+  if (p.zwrap) return wrapi(z, p.nz);
+  return max(-p.G, min(z, p.nz - 1 + p.G));
+}
 
 // 8-byte asynchronous global -> shared copy (LDGSTS); completed with cp.async.wait_group
 __device__ __forceinline__ void cp_async8(double *smem, const double *gmem) {
@@ -199,12 +214,14 @@ template <int M>
 cudaError_t zpass_launch(const KParams &p, const double *q, double *w, double *gz, int zb, int ze,
                          cudaStream_t s) {
   constexpr int smem = zp_smem_bytes<M>();
-  static bool init = false;
-  if (!init) {
-    cudaError_t e =
-        cudaFuncSetAttribute(zpass_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  // symmetry in z (one GPU only) gets its own instantiation: mirrored plane reads
+  const int sz = p.zwrap && p.sym[2] ? 1 : 0;
+  auto kern = sz ? zpass_kernel<M, true> : zpass_kernel<M, false>;
+  static bool init[2] = {false, false};
+  if (!init[sz]) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    init = true;
+    init[sz] = true;
   }
   const int gx = (p.nx + ZP_TX - 1) / ZP_TX, gy = p.ny;
   const int chunks = (ze - zb + ZP_TZ - 1) / ZP_TZ;
@@ -214,7 +231,7 @@ cudaError_t zpass_launch(const KParams &p, const double *q, double *w, double *g
   const int seg_len = ((chunks + nseg - 1) / nseg) * ZP_TZ;
   nseg = (ze - zb + seg_len - 1) / seg_len;
   dim3 grid(gx, gy, nseg);
-  zpass_kernel<M><<<grid, ZP_THREADS, smem, s>>>(p, q, w, gz, zb, ze, seg_len);
+  kern<<<grid, ZP_THREADS, smem, s>>>(p, q, w, gz, zb, ze, seg_len);
   return cudaGetLastError();
 }
 
@@ -227,17 +244,22 @@ cudaError_t xypass_launch(const KParams &p, const double *q, double *qout, doubl
                           cudaStream_t s) {
 #if OSBLI_XY_WS
   constexpr int smem = ws::xy_smem_bytes<M>();
-  static bool init = false;
-  if (!init) {
-    cudaError_t e = cudaFuncSetAttribute(ws::xypass_kernel<M>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int v = (p.two_reg ? 1 : 0) + (p.sym[0] || p.sym[1] ? 2 : 0);
+  auto kern = v == 0 ? ws::xypass_kernel<M, false, false>
+              : v == 1 ? ws::xypass_kernel<M, true, false>
+              : v == 2 ? ws::xypass_kernel<M, false, true>
+                       : ws::xypass_kernel<M, true, true>;
+  static bool init[4] = {false, false, false, false};
+  if (!init[v]) {
+    cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    init = true;
+    init[v] = true;
   }
   const int seg = ze - zb < ws::XY_SEG ? ze - zb : ws::XY_SEG;
   dim3 grid((p.nx + ws::XY_TX - 1) / ws::XY_TX, (p.ny + ws::XY_TY - 1) / ws::XY_TY,
             (ze - zb + seg - 1) / seg);
-  ws::xypass_kernel<M><<<grid, ws::XY_CTA, smem, s>>>(p, q, qout, w, gz, rout, flag, zb, ze, seg);
+  kern<<<grid, ws::XY_CTA, smem, s>>>(p, q, qout, w, gz, rout, flag, zb, ze, seg);
 #else
   constexpr int smem = xy_smem_bytes<M>();
   static bool init = false;

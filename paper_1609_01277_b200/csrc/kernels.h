@@ -23,6 +23,13 @@ struct KParams {
   int read_w, write_w;     // A != 0 ; W needed by a later stage
   const double *src;       // optional steady source S, [nz][5][ny][nx] (dQ/dt = R + S)
   int sym[3];              // 1: symmetry boundaries in direction d, 0: periodic
+  // two-register RK3 (OSBLI_RK3_2R, D-25): the z-pass writes W' = dt Rz into the
+  // interior planes of the destination Q buffer (its `w` argument); the xy-pass
+  // reads W' there and keeps Q_old in its own `w` argument:
+  //   Q' = base + B (W' + dt R_xy),  w <- base + beta (W' + dt R_xy)  (write_w)
+  // with base = w (read_w) or Q.
+  int two_reg;
+  double beta;
 };
 
 // Device buffers of one handle.  Q buffers: [nz + 2G][5][ny][nx] (plane-major,

@@ -60,9 +60,15 @@ __global__ void __launch_bounds__(256) scalar_stage_kernel(const SParams p,
       continue;
     }
     double wn = p.dt * R;
-    if (p.read_w) wn = fma(p.A, w[t], wn);
-    if (p.write_w) w[t] = wn;
-    const double q = fma(p.B, wn, c);
+    double base = c;
+    if (p.two_reg) {
+      if (p.read_w) base = w[t];
+      if (p.write_w) w[t] = fma(p.beta, wn, base);
+    } else {
+      if (p.read_w) wn = fma(p.A, w[t], wn);
+      if (p.write_w) w[t] = wn;
+    }
+    const double q = fma(p.B, wn, base);
     out[t] = q;
     if (!isfinite(q)) atomicOr(flag, 1u);
   }

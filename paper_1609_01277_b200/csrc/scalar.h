@@ -12,6 +12,8 @@ struct SParams {
   double kd;     // diffusivity
   double A, B, dt;
   int read_w, write_w;
+  int two_reg;   // two-register RK3 (D-25): out <- base + B dt R, w <- base + beta dt R,
+  double beta;   // base = w (read_w) or phi
 };
 
 // One stage: W <- A W + dt R(phi), out <- phi + B W; or rout <- R(phi) if rout != null.

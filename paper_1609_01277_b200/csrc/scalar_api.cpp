@@ -66,7 +66,7 @@ int osbli_scalar_create(int nx, int ny, int nz, int order, double dx, double dt,
   if (nx < 1 || ny < 1 || nz < 1 || order < 2 || order % 2 || !(dx > 0) || !std::isfinite(dx) ||
       !(dt > 0) || !std::isfinite(dt) || !std::isfinite(u0) || !std::isfinite(u1) ||
       !std::isfinite(u2) || !(kappa >= 0) || !std::isfinite(kappa) ||
-      (scheme != OSBLI_EULER && scheme != OSBLI_RK3)) {
+      (scheme != OSBLI_EULER && scheme != OSBLI_RK3 && scheme != OSBLI_RK3_2R)) {
     g_scalar_error = "invalid argument";
     return OSBLI_E_INVAL;
   }
@@ -151,12 +151,17 @@ int osbli_scalar_step(osbli_scalar *h, int n) {
   if (h->poisoned) return OSBLI_E_STATE;
   static const double RK_A[3] = {0.0, -5.0 / 9.0, -153.0 / 128.0};
   static const double RK_B[3] = {1.0 / 3.0, 15.0 / 16.0, 8.0 / 15.0};
-  const int ns = h->scheme == OSBLI_RK3 ? 3 : 1;
+  static const double RK2R_ALPHA[3] = {2.0 / 3.0, 5.0 / 12.0, 3.0 / 5.0};
+  static const double RK2R_BETA[3] = {1.0 / 4.0, 3.0 / 20.0, 3.0 / 5.0};
+  const int ns = h->scheme == OSBLI_EULER ? 1 : 3;
   for (int it = 0; it < n; ++it) {
     for (int s = 0; s < ns; ++s) {
       osbli::SParams p = h->base;
       if (h->scheme == OSBLI_RK3) {
         p.A = RK_A[s]; p.B = RK_B[s]; p.read_w = s > 0; p.write_w = s < 2;
+      } else if (h->scheme == OSBLI_RK3_2R) {
+        p.A = 0.0; p.B = RK2R_ALPHA[s]; p.beta = RK2R_BETA[s]; p.two_reg = 1;
+        p.read_w = s > 0; p.write_w = s < 2;
       } else {
         p.A = 0.0; p.B = 1.0; p.read_w = 0; p.write_w = 0;
       }

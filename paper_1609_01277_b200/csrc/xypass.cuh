@@ -207,7 +207,9 @@ __global__ void __launch_bounds__(XY_THREADS, 1)
     if (x < p.nx && y < p.ny) {
       const size_t o = (size_t)z * 5 * FS + (size_t)y * p.nx + x;
 #pragma unroll
-      for (int f = 0; f < 5; ++f) cp_async8(PF + f * XY_TX * XY_TY + lin, w + o + f * FS);
+      for (int f = 0; f < 5; ++f)
+        cp_async8(PF + f * XY_TX * XY_TY + lin,
+                  (p.two_reg ? qout + qplane(p, 0) : w) + o + f * FS);
     }
   }
   asm volatile("cp.async.commit_group;\n" ::: "memory");
@@ -432,8 +434,14 @@ __global__ void __launch_bounds__(XY_THREADS, 1)
         rout[o + f * FS] = wn;
         continue;
       }
-      if (p.write_w) w[o + f * FS] = wn;
-      const double qn = fma(p.B, wn, S[fidx[f] * FSZ + c]);
+      double qb = S[fidx[f] * FSZ + c];
+      if (p.two_reg) {  // W' came from qout's interior planes; w holds Q_old
+        if (p.read_w) qb = w[o + f * FS];
+        if (p.write_w) w[o + f * FS] = fma(p.beta, wn, qb);
+      } else if (p.write_w) {
+        w[o + f * FS] = wn;
+      }
+      const double qn = fma(p.B, wn, qb);
       qo[f * FS] = qn;
       bad |= !isfinite(qn);
     }

@@ -208,7 +208,7 @@ __device__ __forceinline__ void conservative_dir(const KParams &p, const double 
 }
 
 // issue the asynchronous copies of plane z's operands into plane buffer PB
-template <int M>
+template <int M, bool SYM>
 __device__ __forceinline__ void xy_issue_plane(const KParams &p, const double *__restrict__ q,
                                                const double *__restrict__ gz, double *PB, int z,
                                                int x0, int y0, int tid, int nthr) {
@@ -220,8 +220,8 @@ __device__ __forceinline__ void xy_issue_plane(const KParams &p, const double *_
   for (int idx = tid; idx < HY * HX; idx += nthr) {
     const int hy = idx / HX, hx = idx - hy * HX;
     int fx, fy;
-    const size_t off = (size_t)bmap(y0 - M + hy, p.ny, p.sym[1], fy) * p.nx +
-                       bmap(x0 - M + hx, p.nx, p.sym[0], fx);
+    const size_t off = (size_t)bmap_t<SYM>(y0 - M + hy, p.ny, p.sym[1], fy) * p.nx +
+                       bmap_t<SYM>(x0 - M + hx, p.nx, p.sym[0], fx);
     double *d = PB + hy * PX + hx;
 #pragma unroll
     for (int f = 0; f < 5; ++f) cp_async8(d + f * FSZ, qp + f * FS + off);
@@ -230,15 +230,15 @@ __device__ __forceinline__ void xy_issue_plane(const KParams &p, const double *_
   for (int idx = tid; idx < XY_TY * HX; idx += nthr) {
     const int ty = idx / HX, hx = idx - ty * HX;
     int fx, fy;
-    const size_t off = (size_t)bmap(y0 + ty, p.ny, p.sym[1], fy) * p.nx +
-                       bmap(x0 - M + hx, p.nx, p.sym[0], fx);
+    const size_t off = (size_t)bmap_t<SYM>(y0 + ty, p.ny, p.sym[1], fy) * p.nx +
+                       bmap_t<SYM>(x0 - M + hx, p.nx, p.sym[0], fx);
     cp_async8(PB + Gm::PB_G02 + ty * PX + hx, gp + off);
   }
   for (int idx = tid; idx < HY * XY_TX; idx += nthr) {
     const int hy = idx >> 5, tx = idx & 31;
     int fx, fy;
-    const size_t off = (size_t)bmap(y0 - M + hy, p.ny, p.sym[1], fy) * p.nx +
-                       bmap(x0 + tx, p.nx, p.sym[0], fx);
+    const size_t off = (size_t)bmap_t<SYM>(y0 - M + hy, p.ny, p.sym[1], fy) * p.nx +
+                       bmap_t<SYM>(x0 + tx, p.nx, p.sym[0], fx);
     cp_async8(PB + Gm::PB_G12 + hy * Gm::TP + tx, gp + FS + off);
   }
   asm volatile("cp.async.commit_group;\n" ::: "memory");
@@ -281,7 +281,12 @@ __device__ __forceinline__ void xy_prefetch_epilogue(const KParams &p, const dou
   }
 }
 
-template <int M>
+// SYM: symmetry boundaries in x or y (mirror maps and the sign fix-up).
+// TR: two-register RK3 epilogue (OSBLI_RK3_2R, kernels.h): W' is read from the
+// interior planes of qout (where the z-pass left it) and w holds Q_old.  A
+// separate instantiation, so the register-holding preload of Q_old costs the
+// other schemes nothing.
+template <int M, bool TR, bool SYM>
 __global__ void __launch_bounds__(XY_CTA, 1)
     xypass_kernel(const KParams p, const double *__restrict__ q, double *__restrict__ qout,
                   double *__restrict__ w, const double *__restrict__ gz,
@@ -314,10 +319,11 @@ __global__ void __launch_bounds__(XY_CTA, 1)
     for (int i = 0; i < nplanes; ++i) {
       const int b = i & 1;
       if (i >= 2) nbar_sync(4 + b, XY_CTA);
-      xy_issue_plane<M>(p, q, gz, SM + b * Gm::PBSZ, zs + i, x0, y0, lane, XY_PROD);
-      xy_prefetch_epilogue(p, w, zs + i, x0, y0, lane, XY_PROD);
+      xy_issue_plane<M, SYM>(p, q, gz, SM + b * Gm::PBSZ, zs + i, x0, y0, lane, XY_PROD);
+      xy_prefetch_epilogue(p, TR ? qout + qplane(p, 0) : w, zs + i, x0, y0, lane, XY_PROD);
+      if (TR && p.read_w) xy_prefetch_epilogue(p, w, zs + i, x0, y0, lane, XY_PROD);
       asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-      if (p.sym[0] | p.sym[1]) {
+      if (SYM) {
         nbar_sync(7, XY_PROD);  // every producer's copies have landed
         xy_mirror_signs<M>(p, SM + b * Gm::PBSZ, x0, y0, lane, XY_PROD);
       }
@@ -457,10 +463,22 @@ __global__ void __launch_bounds__(XY_CTA, 1)
           const int y = min(y0 + seg * XY_RY + j, p.ny - 1);
           const size_t o = (size_t)z * 5 * FS + (size_t)y * p.nx + (xin ? x : p.nx - 1);
 #pragma unroll
-          for (int f = 0; f < 5; ++f) wp[f][j] = w[o + f * FS];
+          for (int f = 0; f < 5; ++f) wp[f][j] = TR ? qout[qplane(p, 0) + o + f * FS] : w[o + f * FS];
         }
         double R[5][4];
         conservative_dir<M, 1>(p, S, PR, base, PX, R);
+        // two-register RK3: the register Q_old of the four points, loaded before
+        // the hand-over wait so that its latency hides behind it
+        double qold[5][4];
+        if (TR && p.read_w) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int y = min(y0 + seg * XY_RY + j, p.ny - 1);
+            const size_t o = (size_t)z * 5 * FS + (size_t)y * p.nx + (xin ? x : p.nx - 1);
+#pragma unroll
+            for (int f = 0; f < 5; ++f) qold[f][j] = w[o + f * FS];
+          }
+        }
         nbar_sync(6, XY_THREADS);  // group A's parts are in XA
         // ---- epilogue: W <- W' + dt R_xy ; Q' <- Q + B W  (rows of 32 columns; residual
         //      mode: dt = 1, A = 0 so that W' = Rz and R = W' + R_xy)
@@ -482,8 +500,14 @@ __global__ void __launch_bounds__(XY_CTA, 1)
               rout[o + f * FS] = wn;
               continue;
             }
-            if (p.write_w) w[o + f * FS] = wn;
-            const double qn = fma(p.B, wn, S[fidx[f] * FSZ + c]);
+            double qb = S[fidx[f] * FSZ + c];
+            if (TR) {  // w holds Q_old
+              if (p.read_w) qb = qold[f][j];
+              if (p.write_w) w[o + f * FS] = fma(p.beta, wn, qb);
+            } else if (p.write_w) {
+              w[o + f * FS] = wn;
+            }
+            const double qn = fma(p.B, wn, qb);
             qo[f * FS] = qn;
             bad |= !isfinite(qn);
           }

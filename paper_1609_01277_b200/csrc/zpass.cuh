@@ -103,7 +103,7 @@ __device__ __forceinline__ double d2w(const KParams &p, const double (&v)[ZP_RZ 
   return s0 + s1;
 }
 
-template <int M>
+template <int M, bool SYMZ>
 __global__ void __launch_bounds__(ZP_THREADS, 1)
     zpass_kernel(const KParams p, const double *__restrict__ q, double *__restrict__ w,
                  double *__restrict__ gz, int z_begin, int z_end, int seg_len) {
@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(ZP_THREADS, 1)
       if (idx < NR * 32) {
         const int pl = idx >> 5;
         int fl;
-        const double *qp = q + qplane(p, zread(p, zs - M + pl, fl)) + rowoff;
+        const double *qp = q + qplane(p, zread_t<SYMZ>(p, zs - M + pl, fl)) + rowoff;
 #pragma unroll
         for (int f = 0; f < 5; ++f) raw[it][f] = __ldg(qp + f * FS);
         if (fl) raw[it][3] = -raw[it][3];  // rho u_z is odd under a z mirror
@@ -151,7 +151,8 @@ __global__ void __launch_bounds__(ZP_THREADS, 1)
   auto issue_raw = [&](int kk) {
     for (int idx = tid; idx < ZP_TZ * 32; idx += ZP_THREADS) {
       const int j = idx >> 5;
-      const double *qp = q + qplane(p, zread(p, zs + kk * ZP_TZ + M + j)) + rowoff;
+      int fl_;
+      const double *qp = q + qplane(p, zread_t<SYMZ>(p, zs + kk * ZP_TZ + M + j, fl_)) + rowoff;
 #pragma unroll
       for (int f = 0; f < 5; ++f) cp_async8(RB + (f * ZP_TZ + j) * 32 + lane, qp + f * FS);
     }
@@ -173,7 +174,7 @@ __global__ void __launch_bounds__(ZP_THREADS, 1)
         const int z = min(zs + zl0 + j, ze - 1);
         const size_t o = (size_t)z * 5 * FS + (size_t)y * p.nx + x;
 #pragma unroll
-        for (int f = 0; f < 5; ++f) wold[f][j] = p.read_w ? w[o + f * FS] : 0.0;
+        for (int f = 0; f < 5; ++f) wold[f][j] = p.read_w && !p.two_reg ? w[o + f * FS] : 0.0;
       }
     }
     double v[ZP_RZ + 2 * M];
@@ -249,8 +250,8 @@ __global__ void __launch_bounds__(ZP_THREADS, 1)
       for (int idx = tid; idx < ZP_TZ * 32; idx += ZP_THREADS) {
         const int j = idx >> 5;
         const int slot = ((k + 1) * ZP_TZ + 2 * M + j) % NR;
-        int fl;
-        zread(p, zs + (k + 1) * ZP_TZ + M + j, fl);
+        int fl = 0;
+        if (SYMZ) zread(p, zs + (k + 1) * ZP_TZ + M + j, fl);
         const double m2 = RB[(3 * ZP_TZ + j) * 32 + lane];
         zstore<M>(p, S, slot, lane, RB[(0 * ZP_TZ + j) * 32 + lane],
                   RB[(1 * ZP_TZ + j) * 32 + lane], RB[(2 * ZP_TZ + j) * 32 + lane],

@@ -17,6 +17,7 @@ _lib = None
 
 OSBLI_EULER = 0
 OSBLI_RK3 = 1
+OSBLI_RK3_2R = 2
 OSBLI_BC_PERIODIC = 0
 OSBLI_BC_SYMMETRY = 1
 _STATUS = {0: "OK", -1: "E_INVAL", -2: "E_UNSUPPORTED", -3: "E_NOMEM", -4: "E_CUDA",

@@ -59,6 +59,23 @@ def test_scalar_parity_with_oracle(osbli, oracle_lib, order, shape):
     assert np.max(np.abs(s.get_state() - ref)) / np.max(np.abs(ref)) < 1e-12
 
 
+@pytest.mark.parametrize("scheme", [0, 2])
+def test_scalar_schemes_parity(osbli, oracle_lib, scheme):
+    """Forward Euler and the two-register RK3 (N2, D-25) of the scalar solver."""
+    shape = (9, 11, 13)
+    dx, phi = _field(shape, 3)
+    S = 0.1 * np.cos(phi)
+    u, kd, dt = (0.7, -0.4, 0.3), 0.05, 2e-3
+    nz, ny, nx = shape
+    p = oracle_lib.OracleParams(nx, ny, nz, 8, dx, dt=dt)
+    s = osbli.ScalarSolver(nx, ny, nz, 8, dx, dt, u=u, kappa=kd, scheme=scheme)
+    s.set_state(phi)
+    s.set_source(S)
+    s.step(5)
+    ref = oracle_lib.scalar_step(p, u, kd, phi, scheme, 5, S=S)
+    assert np.max(np.abs(s.get_state() - ref)) / np.max(np.abs(ref)) < 1e-12
+
+
 def test_paper_wave_on_gpu(osbli, oracle_lib):
     """P:182-184 on the GPU: 8th order, RK3, dx = 1e-3, dt = 4e-4, t = 1: error O(1e-10)."""
     g = json.load(open(GOLDEN))["wave_1d"]

@@ -48,3 +48,21 @@ def test_loopback_slabs_bitwise_equal_single_domain(osbli, order, nslabs, shape)
     with pytest.raises(osbli.OsbliError):
         grp.slabs[0].step(1)  # members advance together only
     grp.close()
+
+
+@pytest.mark.parametrize("order,nslabs,shape", [(4, 2, (24, 20, 16)), (12, 3, (20, 18, 40))])
+def test_loopback_two_register_rk3(osbli, order, nslabs, shape):
+    """OSBLI_RK3_2R on the ghost-plane path (its z-pass writes into the destination
+    buffer's interior planes; the ghost planes and the split schedule must not care)."""
+    dx = 2 * math.pi / max(shape)
+    dt = 2e-3
+    Q = perturbed_tgv(*shape, dx=dx, amp=0.02)
+    ref = osbli.Solver(*shape, order, dx, dt, scheme=osbli.OSBLI_RK3_2R, **TGV_PHYS)
+    ref.set_state(Q)
+    ref.step(3)
+    grp = osbli.LoopbackGroup(*shape, order, dx, dt, nslabs, scheme=osbli.OSBLI_RK3_2R,
+                              **TGV_PHYS)
+    grp.set_state(Q)
+    grp.step(3)
+    assert np.array_equal(grp.get_state(), ref.get_state())
+    grp.close()
