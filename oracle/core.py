@@ -35,7 +35,9 @@ class _CParams(ctypes.Structure):
     _fields_ = [("nx", ctypes.c_int), ("ny", ctypes.c_int), ("nz", ctypes.c_int),
                 ("order", ctypes.c_int), ("dx", ctypes.c_double), ("dt", ctypes.c_double),
                 ("Re", ctypes.c_double), ("Pr", ctypes.c_double), ("Minf", ctypes.c_double),
-                ("gamma", ctypes.c_double), ("sym", ctypes.c_int * 3)]
+                ("gamma", ctypes.c_double), ("sym", ctypes.c_int * 3),
+                ("energy_form", ctypes.c_int), ("visc_law", ctypes.c_int),
+                ("suth", ctypes.c_double)]
 
 
 @dataclass
@@ -51,10 +53,14 @@ class OracleParams:
     Minf: float = 0.1
     gamma: float = 1.4
     sym: tuple = (0, 0, 0)  # 1: symmetry boundaries in x, y, z; 0: periodic
+    energy_form: int = 0    # 0: expanded viscous work (D-5); 1: conservative (D-27)
+    visc_law: int = 0       # 0: mu = 1 (D-3); 1: Sutherland mu(T) (D-26)
+    suth: float = 0.0       # Sutherland S / T_ref
 
     def c(self) -> _CParams:
         return _CParams(self.nx, self.ny, self.nz, self.order, self.dx, self.dt,
-                        self.Re, self.Pr, self.Minf, self.gamma, (ctypes.c_int * 3)(*self.sym))
+                        self.Re, self.Pr, self.Minf, self.gamma, (ctypes.c_int * 3)(*self.sym),
+                        self.energy_form, self.visc_law, self.suth)
 
     @property
     def shape(self):

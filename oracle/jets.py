@@ -108,10 +108,12 @@ def coordinate_jets(X, Y, Z):
     return out
 
 
-def exact_residual(prim_fn, X, Y, Z, Re, Pr, Minf, gamma):
+def exact_residual(prim_fn, X, Y, Z, Re, Pr, Minf, gamma, suth=None):
     """Exact dQ/dt of eqs. (5)-(7) for the primitive state prim_fn(x, y, z, M).
 
-    Returns [5, ...] (rho, rho u_i, rho E).  mu == 1 (reading D-3).
+    Returns [5, ...] (rho, rho u_i, rho E).  mu == 1 (reading D-3), or, with
+    ``suth`` = S/T_ref, Sutherland's mu(T) = T^1.5 (1 + S)/(T + S) (D-26): only
+    mu and its first derivatives enter, d mu/dx_j = mu'(T) dT/dx_j exactly.
     """
     x, y, z = coordinate_jets(X, Y, Z)
     rho, u0, u1, u2, p = prim_fn(x, y, z, M)
@@ -123,21 +125,28 @@ def exact_residual(prim_fn, X, Y, Z, Re, Pr, Minf, gamma):
     T = p * (gamma * Minf ** 2) / rho  # EOS (10)
     G = [[u[i].g[j] for j in range(3)] for i in range(3)]  # du_i/dx_j
     div = G[0][0] + G[1][1] + G[2][2]
-    tau = [[nu * (G[i][j] + G[j][i] - (2.0 / 3.0 * div if i == j else 0.0)) for j in range(3)]
-           for i in range(3)]
-    # d tau_ij / dx_j = nu (lap u_i + 1/3 d_i div)   (continuous identity)
+    if suth is None:
+        mu, dmu = np.ones_like(T.v), [np.zeros_like(T.v)] * 3
+    else:
+        mu = T.v ** 1.5 * (1.0 + suth) / (T.v + suth)
+        mup = mu * (1.5 / T.v - 1.0 / (T.v + suth))
+        dmu = [mup * T.g[j] for j in range(3)]
+    S = [[G[i][j] + G[j][i] - (2.0 / 3.0 * div if i == j else 0.0) for j in range(3)]
+         for i in range(3)]
+    tau = [[nu * mu * S[i][j] for j in range(3)] for i in range(3)]
+    # d tau_ij / dx_j = nu (mu (lap u_i + 1/3 d_i div) + d_j mu S_ij)  (continuous identity)
     dtau = []
     for i in range(3):
         lap = sum(u[i].h[j, j] for j in range(3))
         ddiv = sum(u[k].h[i, k] for k in range(3))
-        dtau.append(nu * (lap + ddiv / 3.0))
+        dtau.append(nu * (mu * (lap + ddiv / 3.0) + sum(dmu[j] * S[i][j] for j in range(3))))
     R = np.zeros((5,) + X.shape)
     R[0] = -sum(m[j].g[j] for j in range(3))
     for i in range(3):
         conv = sum((m[i] * u[j]).g[j] for j in range(3))
         R[1 + i] = -conv - p.g[i] + dtau[i]
     conv_e = sum(((E + p) * u[j]).g[j] for j in range(3))
-    heat = kap * sum(T.h[j, j] for j in range(3))
+    heat = kap * sum(mu * T.h[j, j] + dmu[j] * T.g[j] for j in range(3))
     # d/dx_j (u_i tau_ij) = tau_ij du_i/dx_j + u_i d tau_ij/dx_j
     visc_work = (sum(tau[i][j] * G[i][j] for i in range(3) for j in range(3))
                  + sum(u[i].v * dtau[i] for i in range(3)))

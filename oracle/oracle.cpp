@@ -240,9 +240,22 @@ double D2(const Grid& g, const double* f, int i, int j, int k, int dir, const Pa
 
 struct Phys {
   double Re, Pr, Minf, gamma;
-  double nu() const { return 1.0 / Re; }  // mu == 1 (D-3); Re = inf -> 0
-  double kappa() const {                   // P:253 heat-flux coefficient, mu == 1
+  int visc_law = 0;     // 0: mu == 1 (D-3); 1: Sutherland mu(T)
+  double suth = 0.0;    // Sutherland constant over the reference temperature, S/T_ref
+  int energy_form = 0;  // 0: viscous work product-rule expanded (D-5); 1: D_j(u_i tau_ij) (N2)
+  double nu() const { return 1.0 / Re; }  // Re = inf -> 0
+  double kappa() const {                   // P:253 heat-flux coefficient without mu
     return 1.0 / ((gamma - 1.0) * Minf * Minf * Pr * Re);
+  }
+  // dimensionless viscosity and its temperature derivative (D-26):
+  //   mu(T) = T^{3/2} (1 + S) / (T + S),  mu(1) = 1
+  double mu(double T) const {
+    if (visc_law == 0) return 1.0;
+    return T * std::sqrt(T) * (1.0 + suth) / (T + suth);
+  }
+  double dmu(double T) const {  // d mu / dT = mu (3/(2T) - 1/(T + S))
+    if (visc_law == 0) return 0.0;
+    return mu(T) * (1.5 / T - 1.0 / (T + suth));
   }
 };
 
@@ -302,6 +315,20 @@ void residual(const Grid& G, const Phys& ph, const double* Q, double* R) {
   Par g_par[3][3];
   for (int i = 0; i < 3; ++i)
     for (int j = 0; j < 3; ++j) g_par[i][j] = odd_in(i) * odd_in(j);
+  // conservative viscous work (N2, D-27): H_j = u_i tau_ij at every point, its
+  // divergence by first-derivative stencils (H_j is odd in direction j)
+  std::vector<double> H[3];
+  if (ph.energy_form == 1) {
+    for (int j = 0; j < 3; ++j) H[j].assign(N, 0.0);
+    for (size_t q = 0; q < N; ++q) {
+      const double div = w.g[0][0][q] + w.g[1][1][q] + w.g[2][2][q];
+      const double mu = ph.mu(w.T[q]);
+      for (int j = 0; j < 3; ++j)
+        for (int i = 0; i < 3; ++i)
+          H[j][q] += w.u[i][q] * (mu * nu *
+                                  (w.g[i][j][q] + w.g[j][i][q] - (i == j ? 2.0 / 3.0 * div : 0.0)));
+    }
+  }
   for (int k = 0; k < G.n[2]; ++k)
     for (int jy = 0; jy < G.n[1]; ++jy)
       for (int ix = 0; ix < G.n[0]; ++ix) {
@@ -327,14 +354,22 @@ void residual(const Grid& G, const Phys& ph, const double* Q, double* R) {
           conv[f] = c;
         }
 
-        // --- stress tensor, eq. (8), P:247-249 (mu == 1):
-        //     tau_ij = (1/Re)(du_i/dx_j + du_j/dx_i - 2/3 delta_ij du_k/dx_k)
+        // --- stress tensor, eq. (8), times the viscosity mu(T) (1, D-3,
+        //     or Sutherland, D-26):
+        //     tau_ij = (mu/Re)(du_i/dx_j + du_j/dx_i - 2/3 delta_ij du_k/dx_k)
         double div = 0.0;
         for (int kk = 0; kk < 3; ++kk) div += g[kk][kk];
-        double tau[3][3];
+        const double mu = ph.mu(w.T[q]);
+        double sij[3][3], tau[3][3];
         for (int i = 0; i < 3; ++i)
-          for (int j = 0; j < 3; ++j)
-            tau[i][j] = nu * (g[i][j] + g[j][i] - (i == j ? 2.0 / 3.0 * div : 0.0));
+          for (int j = 0; j < 3; ++j) {
+            sij[i][j] = g[i][j] + g[j][i] - (i == j ? 2.0 / 3.0 * div : 0.0);
+            tau[i][j] = mu * nu * sij[i][j];
+          }
+        // d mu / dx_j by the chain rule mu'(T) D_j T (D-26); zero for mu == 1
+        double dmu[3] = {0.0, 0.0, 0.0};
+        if (ph.visc_law != 0)
+          for (int j = 0; j < 3; ++j) dmu[j] = ph.dmu(w.T[q]) * D1(G, w.T.data(), ix, jy, k, j);
 
         // --- d tau_ij / dx_j, expanded term by term:
         //   nu [ d2u_i/dx_j dx_j  +  d/dx_j(du_j/dx_i)  -  2/3 d/dx_i(du_k/dx_k) ]
@@ -354,7 +389,10 @@ void residual(const Grid& G, const Phys& ph, const double* Q, double* R) {
             if (kk == i) graddiv += D2(G, w.u[i].data(), ix, jy, k, i, odd_in(i));
             else graddiv += D1(G, w.g[kk][kk].data(), ix, jy, k, i, g_par[kk][kk]);
           }
-          V[i] = nu * (lap + cross - 2.0 / 3.0 * graddiv);
+          // d/dx_j (mu S_ij) = mu dS_ij/dx_j + (d mu/dx_j) S_ij   (product rule, D-26)
+          double gradmu = 0.0;
+          for (int j = 0; j < 3; ++j) gradmu += dmu[j] * sij[i][j];
+          V[i] = nu * (mu * (lap + cross - 2.0 / 3.0 * graddiv) + gradmu);
         }
 
         // --- continuity, eq. (5)
@@ -365,14 +403,21 @@ void residual(const Grid& G, const Phys& ph, const double* Q, double* R) {
         // --- energy, eq. (7): - d/dx_j[rho E u_j + u_j p - q_j - u_i tau_ij]
         //     q_j = kappa dT/dx_j (eq. 9), its divergence by D_jj;
         //     d/dx_j(u_i tau_ij) = tau_ij du_i/dx_j + u_i dtau_ij/dx_j (product rule, D-5)
+        //     with mu(T): d/dx_j(mu dT/dx_j) = mu D_jj T + (d mu/dx_j) D_j T (D-26)
+        //     energy_form 1: d/dx_j(u_i tau_ij) = D_j H_j (N2, D-27)
         double pu = 0.0, heat = 0.0, work = 0.0, uv = 0.0;
         for (int j = 0; j < 3; ++j) {
           pu += D1prod(G, w.p.data(), EVEN, w.u[j].data(), odd_in(j), ix, jy, k, j);
-          heat += D2(G, w.T.data(), ix, jy, k, j);
+          heat += mu * D2(G, w.T.data(), ix, jy, k, j);
+          if (ph.visc_law != 0) heat += dmu[j] * D1(G, w.T.data(), ix, jy, k, j);
         }
-        for (int i = 0; i < 3; ++i) {
-          for (int j = 0; j < 3; ++j) work += tau[i][j] * g[i][j];
-          uv += u[i] * V[i];
+        if (ph.energy_form == 1) {
+          for (int j = 0; j < 3; ++j) work += D1(G, H[j].data(), ix, jy, k, j, odd_in(j));
+        } else {
+          for (int i = 0; i < 3; ++i) {
+            for (int j = 0; j < 3; ++j) work += tau[i][j] * g[i][j];
+            uv += u[i] * V[i];
+          }
         }
         R[4 * N + q] = -conv[4] - pu + kap * heat + work + uv;
       }
@@ -416,13 +461,14 @@ void diagnostics(const Grid& G, const Phys& ph, const double* Q, double out[3]) 
       om2 += om * om;
     }
     ens.add(0.5 * rho * om2);
-    // D-12: viscous dissipation rate tau_ij du_i/dx_j
+    // D-12: viscous dissipation rate tau_ij du_i/dx_j (tau with mu(T), D-26)
     double div = w.g[0][0][q] + w.g[1][1][q] + w.g[2][2][q];
+    const double mu = ph.mu(w.T[q]);
     double phi = 0.0;
     for (int i = 0; i < 3; ++i)
       for (int j = 0; j < 3; ++j) {
         const double tau =
-            nu * (w.g[i][j][q] + w.g[j][i][q] - (i == j ? 2.0 / 3.0 * div : 0.0));
+            mu * nu * (w.g[i][j][q] + w.g[j][i][q] - (i == j ? 2.0 / 3.0 * div : 0.0));
         phi += tau * w.g[i][j][q];
       }
     dis.add(phi);
@@ -453,8 +499,22 @@ extern "C" {
 struct oracle_params {
   int nx, ny, nz, order;
   double dx, dt, Re, Pr, Minf, gamma;
-  int sym[3];  // 1: symmetry boundaries in direction d, 0: periodic
+  int sym[3];       // 1: symmetry boundaries in direction d, 0: periodic
+  int energy_form;  // 0: expanded viscous work (D-5); 1: conservative D_j(u_i tau_ij) (D-27)
+  int visc_law;     // 0: mu == 1 (D-3); 1: Sutherland mu(T) (D-26)
+  double suth;      // Sutherland S / T_ref (visc_law 1)
 };
+
+static bool make_phys(const oracle_params* P, Phys& ph) {
+  ph = Phys{P->Re, P->Pr, P->Minf, P->gamma};
+  if (P->energy_form < 0 || P->energy_form > 1 || P->visc_law < 0 || P->visc_law > 1)
+    return false;
+  if (P->visc_law == 1 && !(P->suth > 0.0)) return false;
+  ph.energy_form = P->energy_form;
+  ph.visc_law = P->visc_law;
+  ph.suth = P->suth;
+  return true;
+}
 
 static bool make_grid(const oracle_params* P, Grid& G) {
   if (!P || P->nx < 1 || P->ny < 1 || P->nz < 1) return false;
@@ -516,7 +576,8 @@ int oracle_derivative(const oracle_params* P, const double* f, int kind, int dir
 int oracle_residual(const oracle_params* P, const double* Q, double* R) {
   Grid G;
   if (!make_grid(P, G)) return -1;
-  Phys ph{P->Re, P->Pr, P->Minf, P->gamma};
+  Phys ph;
+  if (!make_phys(P, ph)) return -1;
   residual(G, ph, Q, R);
   return 0;
 }
@@ -526,7 +587,8 @@ int oracle_residual(const oracle_params* P, const double* Q, double* R) {
 int oracle_step(const oracle_params* P, double* Q, int scheme, int nsteps) {
   Grid G;
   if (!make_grid(P, G) || scheme < 0 || scheme > 2 || nsteps < 0) return -1;
-  Phys ph{P->Re, P->Pr, P->Minf, P->gamma};
+  Phys ph;
+  if (!make_phys(P, ph)) return -1;
   const size_t n5 = 5 * G.npts();
   std::vector<double> R(n5), W(n5, 0.0);
   for (int it = 0; it < nsteps; ++it) {
@@ -560,7 +622,8 @@ int oracle_step(const oracle_params* P, double* Q, int scheme, int nsteps) {
 int oracle_diagnostics(const oracle_params* P, const double* Q, double* out3) {
   Grid G;
   if (!make_grid(P, G)) return -1;
-  Phys ph{P->Re, P->Pr, P->Minf, P->gamma};
+  Phys ph;
+  if (!make_phys(P, ph)) return -1;
   diagnostics(G, ph, Q, out3);
   return 0;
 }
