@@ -52,6 +52,19 @@ typedef struct osbli_ctx osbli_ctx;
  * face, scalars even, the momentum component normal to the face odd. */
 enum { OSBLI_BC_PERIODIC = 0, OSBLI_BC_SYMMETRY = 1 };
 
+/* Viscosity law ("viscosity can be treated either as a
+ * constant or as a spatially-varying term"; D-26): constant mu = 1
+ * (default, D-3), or Sutherland's law in dimensionless form,
+ * mu(T) = T^1.5 (1 + S)/(T + S) with S the Sutherland constant over the
+ * reference temperature (e.g. 110.4 K / 288 K). */
+enum { OSBLI_VISC_CONSTANT = 0, OSBLI_VISC_SUTHERLAND = 1 };
+
+/* Form of the viscous work d/dx_j(u_i tau_ij) in the energy equation (SURVEY
+ * §8(f) N2; D-5, D-27): product-rule expanded tau_ij g_ij + u_i V_i
+ * (default), or conservative, the first-derivative stencil of the pointwise
+ * flux H_j = u_i tau_ij, which conserves total energy to round-off. */
+enum { OSBLI_ENERGY_EXPANDED = 0, OSBLI_ENERGY_CONSERVATIVE = 1 };
+
 /* Time schemes: forward Euler, the 3-stage 2N-storage RK3
  * (Williamson coefficients in Carpenter-Kennedy 2N form; D-1), and
  * the two-register ("SBLI") third-order RK: per stage Q <- Q_old + alpha_s dt R,
@@ -148,6 +161,16 @@ int osbli_diagnostics(osbli_ctx *h, osbli_diag *out);
  * effect at the next stage.  Symmetry in z is not built for slab-decomposed
  * handles (OSBLI_E_UNSUPPORTED). */
 int osbli_set_boundary(osbli_ctx *h, int dir, int bc);
+
+/* Viscosity law (OSBLI_VISC_*); suth = S/T_ref > 0 for Sutherland (ignored for
+ * the constant law).  Takes effect at the next stage; allocates nz*nx*ny doubles
+ * of device scratch for Sutherland.  Diagnostics use the same mu(T). */
+int osbli_set_viscosity(osbli_ctx *h, int law, double suth);
+
+/* Energy-equation form of the viscous work (OSBLI_ENERGY_*).  The conservative
+ * form adds one kernel per stage and 4*nz*nx*ny doubles of device scratch; it is
+ * not built for slab-decomposed handles (OSBLI_E_UNSUPPORTED). */
+int osbli_set_energy_form(osbli_ctx *h, int form);
 
 /* Steady source term S added to the right-hand side, dQ/dt = R(Q) + S (the
  * method of manufactured solutions).  S is

@@ -11,6 +11,10 @@ as device pointers) and process groups (``init_distributed``).
 from .native import (  # noqa: F401
     OSBLI_BC_PERIODIC,
     OSBLI_BC_SYMMETRY,
+    OSBLI_ENERGY_CONSERVATIVE,
+    OSBLI_ENERGY_EXPANDED,
+    OSBLI_VISC_CONSTANT,
+    OSBLI_VISC_SUTHERLAND,
     OSBLI_EULER,
     OSBLI_RK3,
     OSBLI_RK3_2R,

@@ -117,6 +117,9 @@ void free_all(osbli_ctx *h) {
   cudaFree(h->nccl_part);
   cudaFree(h->src);
   h->src = nullptr;
+  cudaFree(h->base.dtz);
+  cudaFree(h->base.hflux);
+  h->base.dtz = h->base.hflux = nullptr;
   h->b = Bufs{};
   h->scratch = nullptr;
   h->nccl_part = nullptr;
@@ -437,6 +440,9 @@ int run_stage(osbli_ctx *h, int s, bool exchange = true) {
     CK(h, osbli::launch_xypass(p, qin, qout, h->b.w, h->b.gz, nullptr, h->b.flag, 0, h->nz,
                                h->stream, &h->launches));
     if (ev) CK(h, cudaEventRecord(ev[2], h->stream));
+    if (p.cons)
+      CK(h, osbli::launch_divh(p, qout, h->b.w, nullptr, h->b.flag, 0, h->nz, h->stream,
+                               &h->launches));
     h->cur ^= 1;
     return OSBLI_OK;
   }
@@ -582,6 +588,42 @@ int osbli_set_boundary(osbli_ctx *h, int dir, int bc) {
   if (dir == 2 && bc == OSBLI_BC_SYMMETRY && h->nranks > 1)
     return fail(h, OSBLI_E_UNSUPPORTED, "symmetry in z is not built for slab decompositions");
   h->base.sym[dir] = bc;
+  return OSBLI_OK;
+}
+
+int osbli_set_viscosity(osbli_ctx *h, int law, double suth) {
+  int u = check_usable(h);
+  if (u) return u;
+  if (law != OSBLI_VISC_CONSTANT && law != OSBLI_VISC_SUTHERLAND)
+    return fail(h, OSBLI_E_INVAL, "bad viscosity law");
+  if (law == OSBLI_VISC_SUTHERLAND && !(suth > 0.0 && std::isfinite(suth)))
+    return fail(h, OSBLI_E_INVAL, "the Sutherland constant must be > 0");
+  const size_t FS = (size_t)h->nx * h->ny;
+  if (law == OSBLI_VISC_SUTHERLAND && !h->base.dtz) {
+    CK(h, cudaStreamSynchronize(h->stream));
+    CK(h, cudaMalloc((void **)&h->base.dtz, (size_t)h->nz * FS * sizeof(double)));
+  }
+  h->base.visc = law;
+  h->base.suth = law == OSBLI_VISC_SUTHERLAND ? suth : 0.0;
+  return OSBLI_OK;
+}
+
+int osbli_set_energy_form(osbli_ctx *h, int form) {
+  int u = check_usable(h);
+  if (u) return u;
+  if (form != OSBLI_ENERGY_EXPANDED && form != OSBLI_ENERGY_CONSERVATIVE)
+    return fail(h, OSBLI_E_INVAL, "bad energy form");
+  if (form == OSBLI_ENERGY_CONSERVATIVE && h->nranks > 1)
+    return fail(h, OSBLI_E_UNSUPPORTED,
+                "the conservative viscous work is not built for slab decompositions");
+  const size_t FS = (size_t)h->nx * h->ny;
+  if (form == OSBLI_ENERGY_CONSERVATIVE) {
+    CK(h, cudaStreamSynchronize(h->stream));
+    if (!h->base.dtz) CK(h, cudaMalloc((void **)&h->base.dtz, (size_t)h->nz * FS * sizeof(double)));
+    if (!h->base.hflux)
+      CK(h, cudaMalloc((void **)&h->base.hflux, (size_t)h->nz * 3 * FS * sizeof(double)));
+  }
+  h->base.cons = form;
   return OSBLI_OK;
 }
 

@@ -90,6 +90,15 @@ __device__ __forceinline__ void cp_async8(double *smem, const double *gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
 }
 
+// Sutherland's law in dimensionless form (D-26): mu(T) = T^1.5 (1 + S)/(T + S),
+// mu(1) = 1, and its derivative mu'(T) = mu (3/(2T) - 1/(T + S))
+__device__ __forceinline__ double sutherland_mu(const KParams &p, double T) {
+  return T * sqrt(T) * (1.0 + p.suth) / (T + p.suth);
+}
+__device__ __forceinline__ double sutherland_dmu(const KParams &p, double T, double mu) {
+  return mu * (1.5 / T - 1.0 / (T + p.suth));
+}
+
 #include "zpass.cuh"
 #include "xypass.cuh"
 #include "xypass_ws.cuh"
@@ -158,8 +167,13 @@ __global__ void __launch_bounds__(256) diag_kernel(const KParams p, const double
     se += 0.5 * rho * (w0 * w0 + w1 * w1 + w2 * w2);
     const double th = g[0][0] + g[1][1] + g[2][2];
     const double s01 = g[0][1] + g[1][0], s02 = g[0][2] + g[2][0], s12 = g[1][2] + g[2][1];
-    sd += p.nu * (2.0 * (g[0][0] * g[0][0] + g[1][1] * g[1][1] + g[2][2] * g[2][2]) +
-                  s01 * s01 + s02 * s02 + s12 * s12 - (2.0 / 3.0) * th * th);
+    double phi = p.nu * (2.0 * (g[0][0] * g[0][0] + g[1][1] * g[1][1] + g[2][2] * g[2][2]) +
+                         s01 * s01 + s02 * s02 + s12 * s12 - (2.0 / 3.0) * th * th);
+    if (p.visc) {  // tau carries mu(T) (D-26)
+      const double pr = p.gm1 * (qp[4 * FS] - 0.5 * rho * (u0 * u0 + u1 * u1 + u2 * u2));
+      phi *= sutherland_mu(p, p.gM2 * pr / rho);
+    }
+    sd += phi;
   }
   // fixed-shape tree reduction -> deterministic, decomposition-independent
   __shared__ double red[3][256];
@@ -180,6 +194,61 @@ __global__ void __launch_bounds__(256) diag_kernel(const KParams p, const double
     part[3 * z + 1] = red[1][0];
     part[3 * z + 2] = red[2][0];
   }
+}
+
+// ------------------------------------------------------------------ conservative viscous work
+// D_j H_j (H_j = u_i tau_ij from the xy-pass; H_j odd under the mirror of
+// direction j) added to the energy of the finished stage (D-27):
+//   residual: R_E += D;  2N: W_E += dt D (write_w), Q'_E += B dt D;
+//   two-register: Q'_E += alpha dt D, Q_old_E += beta dt D (write_w).
+// One thread per point, x fastest; the taps come through L1/L2.
+template <int M>
+__global__ void __launch_bounds__(256) divh_kernel(const KParams p, double *__restrict__ qout,
+                                                   double *__restrict__ w,
+                                                   double *__restrict__ rout,
+                                                   unsigned int *__restrict__ flag, int zb,
+                                                   int ze) {
+  const size_t FS = (size_t)p.nx * p.ny;
+  const size_t n = (size_t)(ze - zb) * FS;
+  const double *H = p.hflux;
+  bool bad = false;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < n;
+       t += (size_t)gridDim.x * blockDim.x) {
+    const int z = zb + (int)(t / FS);
+    const size_t off = t % FS;
+    const int y = (int)(off / p.nx), x = (int)(off % p.nx);
+    const double *hx = H + (size_t)z * 3 * FS + (size_t)y * p.nx;
+    const double *hy = H + (size_t)z * 3 * FS + FS + x;
+    double sx = 0.0, sy = 0.0, sz = 0.0;
+#pragma unroll
+    for (int k = 1; k <= M; ++k) {
+      int f1, f2;
+      const int xp = bmap(x + k, p.nx, p.sym[0], f1), xm = bmap(x - k, p.nx, p.sym[0], f2);
+      sx = fma(p.a[k - 1], (f1 ? -hx[xp] : hx[xp]) - (f2 ? -hx[xm] : hx[xm]), sx);
+      const int yp = bmap(y + k, p.ny, p.sym[1], f1), ym = bmap(y - k, p.ny, p.sym[1], f2);
+      sy = fma(p.a[k - 1],
+               (f1 ? -hy[(size_t)yp * p.nx] : hy[(size_t)yp * p.nx]) -
+                   (f2 ? -hy[(size_t)ym * p.nx] : hy[(size_t)ym * p.nx]),
+               sy);
+      const int zp = zread(p, z + k, f1), zm = zread(p, z - k, f2);
+      const double vp = H[(size_t)zp * 3 * FS + 2 * FS + off],
+                   vm = H[(size_t)zm * 3 * FS + 2 * FS + off];
+      sz = fma(p.a[k - 1], (f1 ? -vp : vp) - (f2 ? -vm : vm), sz);
+    }
+    const double d = sx + sy + sz;
+    const size_t o = (size_t)z * 5 * FS + 4 * FS + off;
+    if (rout) {
+      rout[o] += d;
+      continue;
+    }
+    const double dd = p.dt * d;
+    double *qe = qout + qplane(p, z) + 4 * FS + off;
+    const double qn = fma(p.B, dd, *qe);
+    *qe = qn;
+    bad |= !isfinite(qn);
+    if (p.write_w) w[o] = fma(p.two_reg ? p.beta : 1.0, dd, w[o]);
+  }
+  if (bad) atomicOr(flag, 1u);
 }
 
 // ------------------------------------------------------------------ layout conversion
@@ -215,9 +284,9 @@ cudaError_t zpass_launch(const KParams &p, const double *q, double *w, double *g
                          cudaStream_t s) {
   constexpr int smem = zp_smem_bytes<M>();
   // symmetry in z (one GPU only) gets its own instantiation: mirrored plane reads
-  const int sz = p.zwrap && p.sym[2] ? 1 : 0;
-  auto kern = sz ? zpass_kernel<M, true> : zpass_kernel<M, false>;
-  static bool init[2] = {false, false};
+  const int sz = (p.visc || p.cons) ? 2 : (p.zwrap && p.sym[2] ? 1 : 0);
+  auto kern = sz == 2 ? zpass_kernel<M, 2> : sz == 1 ? zpass_kernel<M, 1> : zpass_kernel<M, 0>;
+  static bool init[3] = {false, false, false};
   if (!init[sz]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
@@ -244,12 +313,13 @@ cudaError_t xypass_launch(const KParams &p, const double *q, double *qout, doubl
                           cudaStream_t s) {
 #if OSBLI_XY_WS
   constexpr int smem = ws::xy_smem_bytes<M>();
-  const int v = (p.two_reg ? 1 : 0) + (p.sym[0] || p.sym[1] ? 2 : 0);
-  auto kern = v == 0 ? ws::xypass_kernel<M, false, false>
-              : v == 1 ? ws::xypass_kernel<M, true, false>
-              : v == 2 ? ws::xypass_kernel<M, false, true>
-                       : ws::xypass_kernel<M, true, true>;
-  static bool init[4] = {false, false, false, false};
+  const int v = (p.visc || p.cons) ? 4 : (p.two_reg ? 1 : 0) + (p.sym[0] || p.sym[1] ? 2 : 0);
+  auto kern = v == 0   ? ws::xypass_kernel<M, 0>
+              : v == 1 ? ws::xypass_kernel<M, 1>
+              : v == 2 ? ws::xypass_kernel<M, 2>
+              : v == 3 ? ws::xypass_kernel<M, 3>
+                       : ws::xypass_kernel<M, 4>;
+  static bool init[5] = {false, false, false, false, false};
   if (!init[v]) {
     cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -337,12 +407,35 @@ cudaError_t launch_xypass(const KParams &p, const double *q_in, double *q_out, d
 #undef XCALL
 }
 
+cudaError_t launch_divh(const KParams &p, double *q_out, double *w, double *r_out,
+                        unsigned int *flag, int zb, int ze, cudaStream_t s, long long *launches) {
+  if (ze <= zb) return cudaSuccess;
+  ++*launches;
+  const size_t n = (size_t)(ze - zb) * p.nx * p.ny;
+  size_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+#define DCALL(MM) divh_kernel<MM><<<(int)blocks, 256, 0, s>>>(p, q_out, w, r_out, flag, zb, ze)
+  switch (p.m) {
+    case 1: DCALL(1); break;
+    case 2: DCALL(2); break;
+    case 3: DCALL(3); break;
+    case 4: DCALL(4); break;
+    case 5: DCALL(5); break;
+    case 6: DCALL(6); break;
+    default: return cudaErrorInvalidValue;
+  }
+#undef DCALL
+  return cudaGetLastError();
+}
+
 cudaError_t launch_stage(const KParams &p, const double *q_in, double *q_out, double *w,
                          double *gz, double *r_out, unsigned int *flag, cudaStream_t s,
                          long long *launches) {
   cudaError_t e = launch_zpass(p, q_in, w, gz, 0, p.nz, s, launches);
   if (e != cudaSuccess) return e;
-  return launch_xypass(p, q_in, q_out, w, gz, r_out, flag, 0, p.nz, s, launches);
+  e = launch_xypass(p, q_in, q_out, w, gz, r_out, flag, 0, p.nz, s, launches);
+  if (e != cudaSuccess || !p.cons) return e;
+  return launch_divh(p, q_out, w, r_out, flag, 0, p.nz, s, launches);
 }
 
 cudaError_t launch_diagnostics(const KParams &p, const double *q_in, double *scratch,

@@ -30,6 +30,12 @@ struct KParams {
   // with base = w (read_w) or Q.
   int two_reg;
   double beta;
+  // equation variants (D-26, D-27)
+  int visc;        // 1: Sutherland mu(T) = T^1.5 (1 + suth)/(T + suth); 0: mu = 1
+  double suth;     // Sutherland constant over the reference temperature
+  int cons;        // 1: viscous work in divergence form D_j H_j, H_j = u_i tau_ij
+  double *dtz;     // variants: D_z T from the z-pass, [nz][ny][nx]
+  double *hflux;   // cons: H_j from the xy-pass, [nz][3][ny][nx]
 };
 
 // Device buffers of one handle.  Q buffers: [nz + 2G][5][ny][nx] (plane-major,
@@ -48,6 +54,12 @@ struct Bufs {
 cudaError_t launch_stage(const KParams &p, const double *q_in, double *q_out, double *w,
                          double *gz, double *r_out, unsigned int *flag, cudaStream_t s,
                          long long *launches);
+
+// Conservative viscous work (p.cons): adds the divergence D_j H_j of the xy-pass's
+// H to the energy of the finished stage (q_out, w) or of the residual (r_out).
+cudaError_t launch_divh(const KParams &p, double *q_out, double *w, double *r_out,
+                        unsigned int *flag, int z_begin, int z_end, cudaStream_t s,
+                        long long *launches);
 
 // z-pass restricted to planes [z_begin, z_end) (for boundary-first overlap).
 cudaError_t launch_zpass(const KParams &p, const double *q_in, double *w, double *gz,

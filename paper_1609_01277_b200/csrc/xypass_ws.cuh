@@ -64,13 +64,14 @@ struct XYGeom {
   static constexpr int PB_G02 = XF_N * FSZ;
   static constexpr int PB_G12 = PB_G02 + XY_TY * PX;
   static constexpr int PBSZ = PB_G12 + EXT;
-  // layout: PB[2] | PR (p, r) | E0 | E1 | XA[5] | XB[5]
+  // layout: PB[2] | PR (p, r) | E0 | E1 | XA[5] | XB[5] | XT
   static constexpr int OFF_PR = 2 * PBSZ;
   static constexpr int OFF_E0 = OFF_PR + 2 * FSZ;   // [HY][TP]   g00 (y-extended)
   static constexpr int OFF_E1 = OFF_E0 + EXT;       // [HY][TP]   g10 (y-extended)
   static constexpr int OFF_XA = OFF_E1 + EXT;       // 5 x [TY][TP]
   static constexpr int OFF_XB = OFF_XA + 5 * NPT;   // 5 x [TY][TP]
-  static constexpr int TOTAL = OFF_XB + 5 * NPT;
+  static constexpr int OFF_XT = OFF_XB + 5 * NPT;   // [TY][TP] D_x T (equation variants)
+  static constexpr int TOTAL = OFF_XT + NPT;
   static constexpr int BYTES = TOTAL * (int)sizeof(double);
 };
 
@@ -122,6 +123,7 @@ __device__ __forceinline__ double wd2(const KParams &p, const double (&v)[W], in
 template <int M>
 struct VelResult {
   double g[3][4], d2u[3][4], d2T[4], mixA[4], mixB[4], mixC[4], mixD[4], uc[3][4];
+  double d1T[4], Tc[4];  // D_d T and T at the outputs (equation variants only)
 };
 
 template <int M, int DIR>
@@ -149,7 +151,11 @@ __device__ __forceinline__ void velocity_dir(const KParams &p, const double *S, 
 #pragma unroll
   for (int k = 0; k < W; ++k) v[k] = __dmul_rn(__dmul_rn(p.gM2, t[k]), r[k]);
 #pragma unroll
-  for (int j = 0; j < 4; ++j) o.d2T[j] = wd2<M, W>(p, v, j);
+  for (int j = 0; j < 4; ++j) {
+    o.d2T[j] = wd2<M, W>(p, v, j);
+    o.d1T[j] = wd1<M, W>(p, v, j);
+    o.Tc[j] = v[j + M];
+  }
   ldwin<W>(S + XF_G22 * Gm::FSZ + base, st, v);  // D_d g22
 #pragma unroll
   for (int j = 0; j < 4; ++j) o.mixA[j] = wd1<M, W>(p, v, j);
@@ -281,23 +287,31 @@ __device__ __forceinline__ void xy_prefetch_epilogue(const KParams &p, const dou
   }
 }
 
-// SYM: symmetry boundaries in x or y (mirror maps and the sign fix-up).
-// TR: two-register RK3 epilogue (OSBLI_RK3_2R, kernels.h): W' is read from the
-// interior planes of qout (where the z-pass left it) and w holds Q_old.  A
-// separate instantiation, so the register-holding preload of Q_old costs the
-// other schemes nothing.
-template <int M, bool TR, bool SYM>
+// Instantiations (XF bits), so that each feature costs the default path nothing:
+// SYM (2): symmetry boundaries in x or y (mirror maps and the sign fix-up).
+// TR (1): two-register RK3 epilogue (OSBLI_RK3_2R, kernels.h): W' is read from
+//   the interior planes of qout (where the z-pass left it) and w holds Q_old.
+// VAR (4): mu(T) (grad-mu terms from D_x T, D_y T and the z-pass's D_z T) and the
+//   conservative viscous work (H_j written for launch_divh); TR and SYM at run time.
+template <int M, int XF>
 __global__ void __launch_bounds__(XY_CTA, 1)
     xypass_kernel(const KParams p, const double *__restrict__ q, double *__restrict__ qout,
                   double *__restrict__ w, const double *__restrict__ gz,
                   double *__restrict__ rout,
                   unsigned int *__restrict__ flag, int z_begin, int z_end, int seg_len) {
+  // XF bits: 1 = two-register epilogue, 2 = symmetry in x/y, 4 = equation variants
+  // (mu(T), conservative viscous work), which take the other two at run time
+  constexpr bool VAR = (XF & 4) != 0;
+  constexpr bool SYM = VAR || (XF & 2) != 0;
+  const bool TR = VAR ? p.two_reg != 0 : (XF & 1) != 0;
+  double *XT = nullptr;
   using Gm = XYGeom<M>;
   constexpr int HX = Gm::HX, HY = Gm::HY, PX = Gm::PX, FSZ = Gm::FSZ, NPT = Gm::NPT, TP = Gm::TP;
   extern __shared__ double SM[];
   double *PR = SM + Gm::OFF_PR;
   double *E0 = SM + Gm::OFF_E0, *E1 = SM + Gm::OFF_E1;
   double *XA = SM + Gm::OFF_XA, *XB = SM + Gm::OFF_XB;
+  XT = SM + Gm::OFF_XT;
   const int tid = threadIdx.x;
   const int x0 = blockIdx.x * XY_TX, y0 = blockIdx.y * XY_TY;
   const int zs = z_begin + blockIdx.z * seg_len;
@@ -323,7 +337,7 @@ __global__ void __launch_bounds__(XY_CTA, 1)
       xy_prefetch_epilogue(p, TR ? qout + qplane(p, 0) : w, zs + i, x0, y0, lane, XY_PROD);
       if (TR && p.read_w) xy_prefetch_epilogue(p, w, zs + i, x0, y0, lane, XY_PROD);
       asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-      if (SYM) {
+      if (SYM && (p.sym[0] | p.sym[1])) {
         nbar_sync(7, XY_PROD);  // every producer's copies have landed
         xy_mirror_signs<M>(p, SM + b * Gm::PBSZ, x0, y0, lane, XY_PROD);
       }
@@ -362,6 +376,26 @@ __global__ void __launch_bounds__(XY_CTA, 1)
         VelResult<M> o;
         velocity_dir<M, 0>(p, S, PR, base, 1, G02 + row * PX + seg * XY_RX, 1, E0, E1, 0, o);
         const double third = 1.0 / 3.0;
+        if (VAR) {
+          // variants: mu(T) scales the viscous parts (D-26); D_x T kept for phase Y;
+          // the conservative form leaves u_i V_i to D_j H_j (D-27)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const double mu = p.visc ? sutherland_mu(p, o.Tc[j]) : 1.0;
+            const double V0 = mu * (p.nu * (o.d2u[0][j] + third * (o.d2u[0][j] + o.mixA[j])));
+            const double V1 = mu * (p.nu * o.d2u[1][j]);
+            const double V2 = mu * (p.nu * (o.d2u[2][j] + third * o.mixB[j]));
+            XA[0 * NPT + pt0 + j] = V0;
+            XA[1 * NPT + pt0 + j] = V1;
+            XA[2 * NPT + pt0 + j] = V2;
+            const double uv = p.cons ? 0.0 : o.uc[0][j] * V0 + o.uc[1][j] * V1 + o.uc[2][j] * V2;
+            XA[3 * NPT + pt0 + j] = fma(p.kappa * mu, o.d2T[j], uv);
+            XA[4 * NPT + pt0 + j] = o.g[2][j];          // g20
+            E0[hy * TP + seg * XY_RX + j] = o.g[0][j];  // g00
+            E1[hy * TP + seg * XY_RX + j] = o.g[1][j];  // g10
+            XT[pt0 + j] = o.d1T[j];
+          }
+        } else
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           // x-parts of V_i: V0 += nu (4/3 D00 u0 + 1/3 D0 g22); V1 += nu D00 u1;
@@ -413,9 +447,74 @@ __global__ void __launch_bounds__(XY_CTA, 1)
       const int base = (seg * XY_RY) * PX + col + M;
       const int ebase = (seg * XY_RY) * TP + col;
       if (grp == 0) {
+        double dTz[4];
+        if (VAR) {  // D_z T of this thread's points (z-pass), loaded ahead of the stencils
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int yy = min(y0 + seg * XY_RY + j, p.ny - 1), xx = min(x0 + col, p.nx - 1);
+            dTz[j] = p.dtz[(size_t)z * FS + (size_t)yy * p.nx + xx];
+          }
+        }
         VelResult<M> o;
         velocity_dir<M, 1>(p, S, PR, base, PX, G12 + ebase, TP, E0, E1, ebase, o);
         const double third = 1.0 / 3.0;
+        if (VAR) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int ty = seg * XY_RY + j;
+            const int pt = ty * TP + col;
+            const int c = (ty + M) * PX + col + M;
+            const double g00 = E0[(ty + M) * TP + col], g10 = E1[(ty + M) * TP + col];
+            const double g20 = XA[4 * NPT + pt];
+            const double g01 = o.g[0][j], g11 = o.g[1][j], g21 = o.g[2][j];
+            const double g02 = G02[ty * PX + col + M], g12 = G12[(ty + M) * TP + col],
+                         g22 = S[XF_G22 * FSZ + c];
+            const double T = o.Tc[j];
+            const double mu = p.visc ? sutherland_mu(p, T) : 1.0;
+            const double dmu = p.visc ? sutherland_dmu(p, T, mu) : 0.0;
+            const double V0y = mu * (p.nu * (o.d2u[0][j] + third * o.mixD[j]));
+            const double V1y =
+                mu * (p.nu * (o.d2u[1][j] + third * (o.d2u[1][j] + o.mixC[j] + o.mixA[j])));
+            const double V2y = mu * (p.nu * (o.d2u[2][j] + third * o.mixB[j]));
+            const double thxy = g00 + g11, th = thxy + g22;
+            const double s01 = g01 + g10, s02 = g02 + g20, s12 = g12 + g21;
+            const double s00 = 2.0 * g00 - (2.0 / 3.0) * th, s11 = 2.0 * g11 - (2.0 / 3.0) * th,
+                         s22 = 2.0 * g22 - (2.0 / 3.0) * th;
+            // grad-mu terms (d mu/dx_j) S_ij, d mu/dx_j = mu'(T) D_j T (D-26)
+            const double tx = XT[pt], ty_ = o.d1T[j], tz = dTz[j];
+            const double cm = p.nu * dmu;
+            const double C0 = cm * (tx * s00 + ty_ * s01 + tz * s02);
+            const double C1 = cm * (tx * s01 + ty_ * s11 + tz * s12);
+            const double C2 = cm * (tx * s02 + ty_ * s12 + tz * s22);
+            const double V0 = XA[0 * NPT + pt] + V0y + C0, V1 = XA[1 * NPT + pt] + V1y + C1,
+                         V2 = XA[2 * NPT + pt] + V2y + C2;
+            const double u0 = o.uc[0][j], u1 = o.uc[1][j], u2 = o.uc[2][j];
+            const double heat =
+                p.kappa * fma(mu, o.d2T[j], dmu * (tx * tx + ty_ * ty_ + tz * tz));
+            double e = XA[3 * NPT + pt] + heat;
+            if (p.cons) {
+              // H_j = u_i tau_ij for the divergence kernel (D-27)
+              const double mn = mu * p.nu;
+              const int y = y0 + ty, x = x0 + col;
+              if (y < p.ny && x < p.nx) {
+                double *h = p.hflux + (size_t)z * 3 * FS + (size_t)y * p.nx + x;
+                h[0] = mn * (u0 * s00 + u1 * s01 + u2 * s02);
+                h[FS] = mn * (u0 * s01 + u1 * s11 + u2 * s12);
+                h[2 * FS] = mn * (u0 * s02 + u1 * s12 + u2 * s22);
+              }
+            } else {
+              const double Phi = mu * (p.nu * (2.0 * (g00 * g00 + g11 * g11 + g22 * g22) +
+                                               s01 * s01 + s02 * s02 + s12 * s12 -
+                                               (2.0 / 3.0) * th * th));
+              e += Phi + (u0 * (V0y + C0) + u1 * (V1y + C1) + u2 * (V2y + C2));
+            }
+            XA[0 * NPT + pt] = -0.5 * S[XF_RHO * FSZ + c] * thxy;
+            XA[1 * NPT + pt] = fma(-0.5 * S[XF_M0 * FSZ + c], thxy, V0);
+            XA[2 * NPT + pt] = fma(-0.5 * S[XF_M1 * FSZ + c], thxy, V1);
+            XA[3 * NPT + pt] = fma(-0.5 * S[XF_M2 * FSZ + c], thxy, V2);
+            XA[4 * NPT + pt] = fma(-0.5 * S[XF_E * FSZ + c], thxy, e);
+          }
+        } else
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const int ty = seg * XY_RY + j;

@@ -103,10 +103,15 @@ __device__ __forceinline__ double d2w(const KParams &p, const double (&v)[ZP_RZ 
   return s0 + s1;
 }
 
-template <int M, bool SYMZ>
+// ZF = 0: periodic z / ghost planes; 1: symmetry in z (mirrored plane reads);
+// 2: equation variants (mu(T), conservative viscous work; D-26, D-27) with
+// run-time boundary handling.  Separate instantiations keep the default path lean.
+template <int M, int ZF>
 __global__ void __launch_bounds__(ZP_THREADS, 1)
     zpass_kernel(const KParams p, const double *__restrict__ q, double *__restrict__ w,
                  double *__restrict__ gz, int z_begin, int z_end, int seg_len) {
+  constexpr bool SYMZ = ZF != 0;
+  constexpr bool VAR = ZF == 2;
   using Zg = ZGeom<M>;
   constexpr int NR = Zg::NR;
   extern __shared__ double S[];
@@ -179,6 +184,41 @@ __global__ void __launch_bounds__(ZP_THREADS, 1)
     }
     double v[ZP_RZ + 2 * M];
     double g[3][ZP_RZ], R[5][ZP_RZ], u2c[ZP_RZ];
+    double dTz[ZP_RZ];
+    if (VAR) {
+      // variants: mu(T) scales the viscous z-parts and the heat flux (D-26; the
+      // grad-mu terms are pointwise and added by the xy-pass from D_z T); the
+      // conservative form leaves the viscous work to D_j H_j (D-27)
+      double mu[ZP_RZ];
+      zwindow<M>(S, ZS_T, slot0, lane, v);
+#pragma unroll
+      for (int j = 0; j < ZP_RZ; ++j) {
+        mu[j] = p.visc ? sutherland_mu(p, v[j + M]) : 1.0;
+        dTz[j] = d1w<M>(p, v, j);
+        R[4][j] = (p.kappa * mu[j]) * d2w<M>(p, v, j);
+      }
+      zwindow<M>(S, ZS_U2, slot0, lane, v);
+#pragma unroll
+      for (int j = 0; j < ZP_RZ; ++j) {
+        g[2][j] = d1w<M>(p, v, j);
+        const double d2u2 = d2w<M>(p, v, j);
+        u2c[j] = v[j + M];
+        const double V2 = mu[j] * (p.nu * (d2u2 + (1.0 / 3.0) * d2u2));
+        R[3][j] = V2;
+        if (!p.cons) R[4][j] = fma(u2c[j], V2, R[4][j]);
+      }
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        zwindow<M>(S, ZS_U0 + i, slot0, lane, v);
+#pragma unroll
+        for (int j = 0; j < ZP_RZ; ++j) {
+          g[i][j] = d1w<M>(p, v, j);
+          const double Vi = mu[j] * (p.nu * d2w<M>(p, v, j));
+          R[1 + i][j] = Vi;
+          if (!p.cons) R[4][j] = fma(v[j + M], Vi, R[4][j]);
+        }
+      }
+    } else {
     // velocity: g_i2 = D_z u_i, z-Laplacian parts of V_i and u_i V_i
     zwindow<M>(S, ZS_U2, slot0, lane, v);
 #pragma unroll
@@ -205,6 +245,7 @@ __global__ void __launch_bounds__(ZP_THREADS, 1)
     zwindow<M>(S, ZS_T, slot0, lane, v);
 #pragma unroll
     for (int j = 0; j < ZP_RZ; ++j) R[4][j] = fma(p.kappa, d2w<M>(p, v, j), R[4][j]);
+    }
     // skew advective + dilatation halves: -1/2 (u_2 D_z s + s g_22), s = rho, m_i, e
 #pragma unroll
     for (int f = 0; f < 5; ++f) {
@@ -240,6 +281,7 @@ __global__ void __launch_bounds__(ZP_THREADS, 1)
           const size_t og = (size_t)z * 3 * FS + (size_t)y * p.nx + x;
 #pragma unroll
           for (int i = 0; i < 3; ++i) gz[og + i * FS] = g[i][j];
+          if (VAR) p.dtz[(size_t)z * FS + (size_t)y * p.nx + x] = dTz[j];
         }
       }
     }

@@ -20,6 +20,10 @@ OSBLI_RK3 = 1
 OSBLI_RK3_2R = 2
 OSBLI_BC_PERIODIC = 0
 OSBLI_BC_SYMMETRY = 1
+OSBLI_VISC_CONSTANT = 0
+OSBLI_VISC_SUTHERLAND = 1
+OSBLI_ENERGY_EXPANDED = 0
+OSBLI_ENERGY_CONSERVATIVE = 1
 _STATUS = {0: "OK", -1: "E_INVAL", -2: "E_UNSUPPORTED", -3: "E_NOMEM", -4: "E_CUDA",
            -5: "E_COMM", -6: "E_NONFINITE", -7: "E_STATE"}
 
@@ -84,6 +88,8 @@ def load():
     L.osbli_loopback_step.argtypes = [ctypes.POINTER(H), c_int, c_int]
     L.osbli_set_source.argtypes = [H, vp, c_int]
     L.osbli_set_boundary.argtypes = [H, c_int, c_int]
+    L.osbli_set_viscosity.argtypes = [H, c_int, ctypes.c_double]
+    L.osbli_set_energy_form.argtypes = [H, c_int]
     L.osbli_scalar_create.argtypes = [c_int, c_int, c_int, c_int, c_double, c_double, c_double,
                                       c_double, c_double, c_double, c_int, ctypes.POINTER(H)]
     for fn in ("osbli_scalar_set_state", "osbli_scalar_set_source", "osbli_scalar_get_state",
@@ -224,6 +230,14 @@ class Solver:
     def set_boundary(self, direction: int, bc: int):
         """OSBLI_BC_PERIODIC or OSBLI_BC_SYMMETRY for direction 0/1/2."""
         self._check(self._L.osbli_set_boundary(self._h, int(direction), int(bc)))
+
+    def set_viscosity(self, law: int, suth: float = 0.0):
+        """OSBLI_VISC_CONSTANT (mu = 1) or OSBLI_VISC_SUTHERLAND with suth = S/T_ref."""
+        self._check(self._L.osbli_set_viscosity(self._h, int(law), float(suth)))
+
+    def set_energy_form(self, form: int):
+        """OSBLI_ENERGY_EXPANDED or OSBLI_ENERGY_CONSERVATIVE viscous work."""
+        self._check(self._L.osbli_set_energy_form(self._h, int(form)))
 
     def set_source(self, S):
         """Steady source: dQ/dt = R(Q) + S (None removes it)."""
