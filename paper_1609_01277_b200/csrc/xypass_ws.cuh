@@ -34,8 +34,9 @@ constexpr int XY_THREADS = 256;          // consumer threads
 #endif
 constexpr int XY_PROD = 32 * OSBLI_XY_PRODUCERS;  // producer threads
 constexpr int XY_CTA = XY_THREADS + XY_PROD;
-// named barriers: 1 = consumers only; 2 + b = buffer b full; 4 + b = buffer b empty;
-// 6 = group A -> group B hand-over at the end of phase Y
+// named barriers: 2 + b = buffer b full (producers -> group A); 4 + b = buffer b
+// empty (consumers -> producers); 7 = producers only; 1, 6, 8, 9, 10: consumers
+// (see the consumer loop)
 __device__ __forceinline__ void nbar_sync(int id, int count) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
 }
@@ -341,7 +342,7 @@ __global__ void __launch_bounds__(XY_CTA, 1)
         nbar_sync(7, XY_PROD);  // every producer's copies have landed
         xy_mirror_signs<M>(p, SM + b * Gm::PBSZ, x0, y0, lane, XY_PROD);
       }
-      nbar_arrive(2 + b, XY_CTA);
+      nbar_arrive(2 + b, XY_PROD + 128);  // producers + group A
     }
     return;
   }
@@ -349,33 +350,46 @@ __global__ void __launch_bounds__(XY_CTA, 1)
 #if OSBLI_XY_PRODUCERS == 4
   asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
 #endif
-  for (int z = zs; z < ze; ++z) {
-    const int i = z - zs, cur = i & 1;
-    double *S = SM + cur * Gm::PBSZ;  // this plane's buffer
-    const double *G02 = S + Gm::PB_G02, *G12 = S + Gm::PB_G12;
-    // ---- plane z landed (producer): formulas p and 1/rho once per point
-    nbar_sync(2 + cur, XY_CTA);
-    for (int idx = tid; idx < HY * HX; idx += XY_THREADS) {
-      const int hy = idx / HX, hx = idx - hy * HX;
-      const int s = hy * PX + hx;
-      const double rho = S[XF_RHO * FSZ + s], m0 = S[XF_M0 * FSZ + s], m1 = S[XF_M1 * FSZ + s],
-                   m2 = S[XF_M2 * FSZ + s], e = S[XF_E * FSZ + s];
-      const double r = 1.0 / rho;
-      PR[XP_P * FSZ + s] = p.gm1 * (e - 0.5 * r * (m0 * m0 + m1 * m1 + m2 * m2));
-      PR[XP_R * FSZ + s] = r;
-    }
-    nbar_sync(1, XY_THREADS);
-
-    // ---- phase X: thread -> (row, 4-wide x segment); lanes 0-15 / 16-31 = 16 rows
-    {
-      const int row = q7 & 15, seg = q7 >> 4;
-      const int hy = row + M;
-      const int base = hy * PX + seg * XY_RX;  // window start (halo coords)
-      const int pt0 = row * TP + seg * XY_RX;
-      if (grp == 0) {
+  // The two consumer groups run decoupled, one plane apart at most; they meet only
+  // where data passes between them (named barriers, arrive -> sync):
+  //   8  A -> B  PR (p, 1/rho) of the plane is ready        (A computes PR)
+  //   9  B -> A  B has read PR: A may compute the next plane's
+  //   6  A -> B  A's parts of every point are in XA
+  //   10 B -> A  B's epilogue has read XA: A may overwrite it
+  //   1  A only  PR complete before phase X; E0/E1/XA[4] of phase X before phase Y
+  // so A's formulas for plane z+1 overlap B's epilogue of plane z.
+  const double third = 1.0 / 3.0;
+  if (grp == 0) {
+    // formulas p and 1/rho once per point of a landed plane buffer
+    auto formulas = [&](const double *Sb) {
+      for (int idx = q7; idx < HY * HX; idx += 128) {
+        const int hy = idx / HX, hx = idx - hy * HX;
+        const int s = hy * PX + hx;
+        const double rho = Sb[XF_RHO * FSZ + s], m0 = Sb[XF_M0 * FSZ + s],
+                     m1 = Sb[XF_M1 * FSZ + s], m2 = Sb[XF_M2 * FSZ + s], e = Sb[XF_E * FSZ + s];
+        const double r = 1.0 / rho;
+        PR[XP_P * FSZ + s] = p.gm1 * (e - 0.5 * r * (m0 * m0 + m1 * m1 + m2 * m2));
+        PR[XP_R * FSZ + s] = r;
+      }
+    };
+    nbar_sync(2, XY_PROD + 128);  // first plane landed
+    formulas(SM);
+    for (int z = zs; z < ze; ++z) {
+      const int i = z - zs, cur = i & 1;
+      double *S = SM + cur * Gm::PBSZ;  // this plane's buffer
+      const double *G02 = S + Gm::PB_G02, *G12 = S + Gm::PB_G12;
+      nbar_sync(1, 128);           // every A thread's PR entries are written
+      nbar_arrive(8, XY_THREADS);  // PR of plane z is complete
+      // ---- phase X: thread -> (row, 4-wide x segment); lanes 0-15 / 16-31 = 16 rows
+      {
+        const int row = q7 & 15, seg = q7 >> 4;
+        const int hy = row + M;
+        const int base = hy * PX + seg * XY_RX;  // window start (halo coords)
+        const int pt0 = row * TP + seg * XY_RX;
         VelResult<M> o;
         velocity_dir<M, 0>(p, S, PR, base, 1, G02 + row * PX + seg * XY_RX, 1, E0, E1, 0, o);
-        const double third = 1.0 / 3.0;
+        // B has finished reading XA (its epilogue of the previous plane)
+        if (i > 0) nbar_sync(10, XY_THREADS);
         if (VAR) {
           // variants: mu(T) scales the viscous parts (D-26); D_x T kept for phase Y;
           // the conservative form leaves u_i V_i to D_j H_j (D-27)
@@ -412,41 +426,31 @@ __global__ void __launch_bounds__(XY_CTA, 1)
           E0[hy * TP + seg * XY_RX + j] = o.g[0][j];  // g00
           E1[hy * TP + seg * XY_RX + j] = o.g[1][j];  // g10
         }
-      } else {
-        double R[5][4];
-        conservative_dir<M, 0>(p, S, PR, base, 1, R);
-#pragma unroll
-        for (int f = 0; f < 5; ++f)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) XB[f * NPT + pt0 + j] = R[f][j];
       }
-    }
-    // ---- g00, g10 on the 2m halo rows (inner derivatives of D_y g00, D_y g10)
-    for (int task = tid; task < 2 * M * (XY_TX / XY_RX); task += XY_THREADS) {
-      const int rr = task % (2 * M), seg = task / (2 * M);
-      const int hy = rr < M ? rr : rr + XY_TY;
-      const int base = hy * PX + seg * XY_RX;
-      constexpr int W = Gm::W;
-      double r[W], v[W], t[W];
-      ldwin<W>(PR + XP_R * FSZ + base, 1, r);
+      // ---- g00, g10 on the 2m halo rows (inner derivatives of D_y g00, D_y g10)
+      for (int task = q7; task < 2 * M * (XY_TX / XY_RX); task += 128) {
+        const int rr = task % (2 * M), seg = task / (2 * M);
+        const int hy = rr < M ? rr : rr + XY_TY;
+        const int base = hy * PX + seg * XY_RX;
+        constexpr int W = Gm::W;
+        double r[W], v[W], t[W];
+        ldwin<W>(PR + XP_R * FSZ + base, 1, r);
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        ldwin<W>(S + (XF_M0 + i) * FSZ + base, 1, t);
+        for (int i = 0; i < 2; ++i) {
+          ldwin<W>(S + (XF_M0 + i) * FSZ + base, 1, t);
 #pragma unroll
-        for (int k = 0; k < W; ++k) v[k] = __dmul_rn(t[k], r[k]);
-        double *Ei = i == 0 ? E0 : E1;
+          for (int k = 0; k < W; ++k) v[k] = __dmul_rn(t[k], r[k]);
+          double *Ei = i == 0 ? E0 : E1;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) Ei[hy * TP + seg * XY_RX + j] = wd1<M, W>(p, v, j);
+          for (int j = 0; j < 4; ++j) Ei[hy * TP + seg * XY_RX + j] = wd1<M, W>(p, v, j);
+        }
       }
-    }
-    nbar_sync(1, XY_THREADS);
-
-    // ---- phase Y: thread -> (column, 4-tall y segment); lanes = 32 consecutive columns
-    {
-      const int col = q7 & 31, seg = q7 >> 5;
-      const int base = (seg * XY_RY) * PX + col + M;
-      const int ebase = (seg * XY_RY) * TP + col;
-      if (grp == 0) {
+      nbar_sync(1, 128);
+      // ---- phase Y: thread -> (column, 4-tall y segment); lanes = 32 consecutive columns
+      {
+        const int col = q7 & 31, seg = q7 >> 5;
+        const int base = (seg * XY_RY) * PX + col + M;
+        const int ebase = (seg * XY_RY) * TP + col;
         double dTz[4];
         if (VAR) {  // D_z T of this thread's points (z-pass), loaded ahead of the stencils
 #pragma unroll
@@ -457,7 +461,6 @@ __global__ void __launch_bounds__(XY_CTA, 1)
         }
         VelResult<M> o;
         velocity_dir<M, 1>(p, S, PR, base, PX, G12 + ebase, TP, E0, E1, ebase, o);
-        const double third = 1.0 / 3.0;
         if (VAR) {
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
@@ -548,10 +551,37 @@ __global__ void __launch_bounds__(XY_CTA, 1)
                                  ex + fma(p.kappa, o.d2T[j], Phi) +
                                      (u0 * V0y + u1 * V1y + u2 * V2y));
         }
-        // A's part of every point of this tile is final: hand over to group B
-        nbar_arrive(6, XY_THREADS);
-        if (i + 2 < nplanes) nbar_arrive(4 + cur, XY_CTA);  // done with this plane buffer
-      } else {
+      }
+      // A's part of every point of this tile is final: hand over to group B
+      nbar_arrive(6, XY_THREADS);
+      if (i + 2 < nplanes) nbar_arrive(4 + cur, XY_CTA);  // done with this plane buffer
+      if (i + 1 < nplanes) {
+        nbar_sync(9, XY_THREADS);                 // B has read PR of plane z
+        nbar_sync(2 + (cur ^ 1), XY_PROD + 128);  // plane z+1 landed
+        formulas(SM + (cur ^ 1) * Gm::PBSZ);
+      }
+    }
+  } else {
+    for (int z = zs; z < ze; ++z) {
+      const int i = z - zs, cur = i & 1;
+      const double *S = SM + cur * Gm::PBSZ;  // this plane's buffer
+      nbar_sync(8, XY_THREADS);  // plane z landed and its PR computed (group A)
+      // ---- phase X: x-derivatives of the conservative group
+      {
+        const int row = q7 & 15, seg = q7 >> 4;
+        const int base = (row + M) * PX + seg * XY_RX;
+        const int pt0 = row * TP + seg * XY_RX;
+        double R[5][4];
+        conservative_dir<M, 0>(p, S, PR, base, 1, R);
+#pragma unroll
+        for (int f = 0; f < 5; ++f)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) XB[f * NPT + pt0 + j] = R[f][j];
+      }
+      // ---- phase Y and the epilogue
+      {
+        const int col = q7 & 31, seg = q7 >> 5;
+        const int base = (seg * XY_RY) * PX + col + M;
         // group B finishes the stage for its 4 points: W' (z-pass output) is loaded
         // first so that its latency hides behind the y-derivatives
         const int x = x0 + col;
@@ -566,6 +596,7 @@ __global__ void __launch_bounds__(XY_CTA, 1)
         }
         double R[5][4];
         conservative_dir<M, 1>(p, S, PR, base, PX, R);
+        if (i + 1 < nplanes) nbar_arrive(9, XY_THREADS);  // done with PR: A may refill it
         // two-register RK3: the register Q_old of the four points, loaded before
         // the hand-over wait so that its latency hides behind it
         double qold[5][4];
@@ -578,7 +609,7 @@ __global__ void __launch_bounds__(XY_CTA, 1)
             for (int f = 0; f < 5; ++f) qold[f][j] = w[o + f * FS];
           }
         }
-        nbar_sync(6, XY_THREADS);  // group A's parts are in XA
+        nbar_sync(6, XY_THREADS);  // group A's parts are in XA (and XB of all B threads)
         // ---- epilogue: W <- W' + dt R_xy ; Q' <- Q + B W  (rows of 32 columns; residual
         //      mode: dt = 1, A = 0 so that W' = Rz and R = W' + R_xy)
         const int fidx[5] = {XF_RHO, XF_M0, XF_M1, XF_M2, XF_E};
@@ -611,6 +642,7 @@ __global__ void __launch_bounds__(XY_CTA, 1)
             bad |= !isfinite(qn);
           }
         }
+        if (i + 1 < nplanes) nbar_arrive(10, XY_THREADS);  // done with XA
         if (i + 2 < nplanes) nbar_arrive(4 + cur, XY_CTA);  // done with this plane buffer
       }
     }

@@ -281,3 +281,21 @@ def test_two_register_rk3_parity(osbli, orc, order, shape):
     s.set_state(Q)
     assert np.all(relerr(s.residual(), orc.residual(orc.OracleParams(*shape, order, dx,
                                                                      **TGV_PHYS), Q)) < TOL)
+
+
+@pytest.mark.parametrize("order,shape", [(2, (40, 36, 33)), (4, (64, 64, 64)), (12, (72, 40, 50))])
+def test_kernels_are_deterministic(osbli, order, shape):
+    """Repeated evaluations are bitwise identical (a race between the xy-pass's
+    warp groups shows up here first, as run-to-run differences)."""
+    dx = 2 * math.pi / max(shape)
+    Q = perturbed_tgv(*shape, dx=dx, amp=0.02)
+    s = make(osbli, shape, order, dx, 1e-3)
+    s.set_state(Q)
+    R0 = s.residual()
+    for _ in range(4):
+        assert np.array_equal(s.residual(), R0)
+    s.step(2)
+    Q2 = s.get_state()
+    s.set_state(Q)
+    s.step(2)
+    assert np.array_equal(s.get_state(), Q2)
