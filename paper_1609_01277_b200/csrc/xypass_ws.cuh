@@ -127,7 +127,9 @@ struct VelResult {
   double d1T[4], Tc[4];  // D_d T and T at the outputs (equation variants only)
 };
 
-template <int M, int DIR>
+// TW: also the temperature stencils (heat flux, and D_d T, T for the variants);
+// without them the heat flux is group B's (conservative_dir<.., HEAT = true>)
+template <int M, int DIR, bool TW>
 __device__ __forceinline__ void velocity_dir(const KParams &p, const double *S, const double *PR,
                                              int base, int st, const double *gmix, int gst,
                                              const double *E0, const double *E1, int ebase,
@@ -148,14 +150,16 @@ __device__ __forceinline__ void velocity_dir(const KParams &p, const double *S, 
       o.uc[i][j] = v[j + M];
     }
   }
-  ldwin<W>(PR + XP_P * Gm::FSZ + base, st, t);
+  if (TW) {
+    ldwin<W>(PR + XP_P * Gm::FSZ + base, st, t);
 #pragma unroll
-  for (int k = 0; k < W; ++k) v[k] = __dmul_rn(__dmul_rn(p.gM2, t[k]), r[k]);
+    for (int k = 0; k < W; ++k) v[k] = __dmul_rn(__dmul_rn(p.gM2, t[k]), r[k]);
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    o.d2T[j] = wd2<M, W>(p, v, j);
-    o.d1T[j] = wd1<M, W>(p, v, j);
-    o.Tc[j] = v[j + M];
+    for (int j = 0; j < 4; ++j) {
+      o.d2T[j] = wd2<M, W>(p, v, j);
+      o.d1T[j] = wd1<M, W>(p, v, j);
+      o.Tc[j] = v[j + M];
+    }
   }
   ldwin<W>(S + XF_G22 * Gm::FSZ + base, st, v);  // D_d g22
 #pragma unroll
@@ -176,13 +180,16 @@ __device__ __forceinline__ void velocity_dir(const KParams &p, const double *S, 
 // Conservative group, one direction d: the d-part of
 //   -[ D_d F_id + 1/2 u_d D_d s ]  (and mass: -1/2 (D_d m_d + u_d D_d rho)),
 //   F_id = 1/2 m_i u_d + delta_id p,  G_d = (1/2 e + p) u_d   (skew halves + pressure)
-template <int M, int DIR>
+// HEAT: also the d-part of the heat flux, kappa D_dd T, from the
+// p and 1/rho windows this group has loaded anyway
+template <int M, int DIR, bool HEAT>
 __device__ __forceinline__ void conservative_dir(const KParams &p, const double *S,
                                                  const double *PR, int base, int st,
                                                  double (&R)[5][4]) {
   using Gm = XYGeom<M>;
   constexpr int W = Gm::W;
   double ud[W], pw[W], v[W], t[W];
+  double heat[4];
   {
     double r[W];
     ldwin<W>(PR + XP_R * Gm::FSZ + base, st, r);
@@ -191,11 +198,17 @@ __device__ __forceinline__ void conservative_dir(const KParams &p, const double 
     for (int k = 0; k < W; ++k) ud[k] = __dmul_rn(t[k], r[k]);
 #pragma unroll
     for (int j = 0; j < 4; ++j) R[0][j] = -0.5 * wd1<M, W>(p, t, j);
+    ldwin<W>(PR + XP_P * Gm::FSZ + base, st, pw);
+    if (HEAT) {
+#pragma unroll
+      for (int k = 0; k < W; ++k) v[k] = __dmul_rn(__dmul_rn(p.gM2, pw[k]), r[k]);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) heat[j] = p.kappa * wd2<M, W>(p, v, j);
+    }
   }
   ldwin<W>(S + XF_RHO * Gm::FSZ + base, st, v);
 #pragma unroll
   for (int j = 0; j < 4; ++j) R[0][j] = fma(-0.5 * ud[j + M], wd1<M, W>(p, v, j), R[0][j]);
-  ldwin<W>(PR + XP_P * Gm::FSZ + base, st, pw);
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
     ldwin<W>(S + (XF_M0 + i) * Gm::FSZ + base, st, v);
@@ -212,6 +225,10 @@ __device__ __forceinline__ void conservative_dir(const KParams &p, const double 
 #pragma unroll
   for (int j = 0; j < 4; ++j)
     R[4][j] = -fma(0.5 * ud[j + M], wd1<M, W>(p, v, j), wd1<M, W>(p, t, j));
+  if (HEAT) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) R[4][j] += heat[j];
+  }
 }
 
 // issue the asynchronous copies of plane z's operands into plane buffer PB
@@ -387,7 +404,7 @@ __global__ void __launch_bounds__(XY_CTA, 1)
         const int base = hy * PX + seg * XY_RX;  // window start (halo coords)
         const int pt0 = row * TP + seg * XY_RX;
         VelResult<M> o;
-        velocity_dir<M, 0>(p, S, PR, base, 1, G02 + row * PX + seg * XY_RX, 1, E0, E1, 0, o);
+        velocity_dir<M, 0, VAR>(p, S, PR, base, 1, G02 + row * PX + seg * XY_RX, 1, E0, E1, 0, o);
         // B has finished reading XA (its epilogue of the previous plane)
         if (i > 0) nbar_sync(10, XY_THREADS);
         if (VAR) {
@@ -420,8 +437,7 @@ __global__ void __launch_bounds__(XY_CTA, 1)
           XA[0 * NPT + pt0 + j] = V0;
           XA[1 * NPT + pt0 + j] = V1;
           XA[2 * NPT + pt0 + j] = V2;
-          XA[3 * NPT + pt0 + j] =
-              fma(p.kappa, o.d2T[j], o.uc[0][j] * V0 + o.uc[1][j] * V1 + o.uc[2][j] * V2);
+          XA[3 * NPT + pt0 + j] = o.uc[0][j] * V0 + o.uc[1][j] * V1 + o.uc[2][j] * V2;
           XA[4 * NPT + pt0 + j] = o.g[2][j];          // g20
           E0[hy * TP + seg * XY_RX + j] = o.g[0][j];  // g00
           E1[hy * TP + seg * XY_RX + j] = o.g[1][j];  // g10
@@ -460,7 +476,7 @@ __global__ void __launch_bounds__(XY_CTA, 1)
           }
         }
         VelResult<M> o;
-        velocity_dir<M, 1>(p, S, PR, base, PX, G12 + ebase, TP, E0, E1, ebase, o);
+        velocity_dir<M, 1, VAR>(p, S, PR, base, PX, G12 + ebase, TP, E0, E1, ebase, o);
         if (VAR) {
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
@@ -541,15 +557,14 @@ __global__ void __launch_bounds__(XY_CTA, 1)
           const double Phi = p.nu * (2.0 * (g00 * g00 + g11 * g11 + g22 * g22) + s01 * s01 +
                                      s02 * s02 + s12 * s12 - (2.0 / 3.0) * th * th);
           const double u0 = o.uc[0][j], u1 = o.uc[1][j], u2 = o.uc[2][j];
-          const double ex = XA[3 * NPT + pt];  // kappa D00 T + u_i V_i^x (phase X)
+          const double ex = XA[3 * NPT + pt];  // u_i V_i^x (phase X; the heat flux is B's)
           // dilatation halves of the skew terms, -1/2 s (g00 + g11)
           XA[0 * NPT + pt] = -0.5 * S[XF_RHO * FSZ + c] * thxy;
           XA[1 * NPT + pt] = fma(-0.5 * S[XF_M0 * FSZ + c], thxy, V0);
           XA[2 * NPT + pt] = fma(-0.5 * S[XF_M1 * FSZ + c], thxy, V1);
           XA[3 * NPT + pt] = fma(-0.5 * S[XF_M2 * FSZ + c], thxy, V2);
           XA[4 * NPT + pt] = fma(-0.5 * S[XF_E * FSZ + c], thxy,
-                                 ex + fma(p.kappa, o.d2T[j], Phi) +
-                                     (u0 * V0y + u1 * V1y + u2 * V2y));
+                                 (ex + Phi) + (u0 * V0y + u1 * V1y + u2 * V2y));
         }
       }
       // A's part of every point of this tile is final: hand over to group B
@@ -572,7 +587,7 @@ __global__ void __launch_bounds__(XY_CTA, 1)
         const int base = (row + M) * PX + seg * XY_RX;
         const int pt0 = row * TP + seg * XY_RX;
         double R[5][4];
-        conservative_dir<M, 0>(p, S, PR, base, 1, R);
+        conservative_dir<M, 0, !VAR>(p, S, PR, base, 1, R);
 #pragma unroll
         for (int f = 0; f < 5; ++f)
 #pragma unroll
@@ -595,7 +610,7 @@ __global__ void __launch_bounds__(XY_CTA, 1)
           for (int f = 0; f < 5; ++f) wp[f][j] = TR ? qout[qplane(p, 0) + o + f * FS] : w[o + f * FS];
         }
         double R[5][4];
-        conservative_dir<M, 1>(p, S, PR, base, PX, R);
+        conservative_dir<M, 1, !VAR>(p, S, PR, base, PX, R);
         if (i + 1 < nplanes) nbar_arrive(9, XY_THREADS);  // done with PR: A may refill it
         // two-register RK3: the register Q_old of the four points, loaded before
         // the hand-over wait so that its latency hides behind it
