@@ -201,52 +201,118 @@ __global__ void __launch_bounds__(256) diag_kernel(const KParams p, const double
 // direction j) added to the energy of the finished stage (D-27):
 //   residual: R_E += D;  2N: W_E += dt D (write_w), Q'_E += B dt D;
 //   two-register: Q'_E += alpha dt D, Q_old_E += beta dt D (write_w).
-// One thread per point, x fastest; the taps come through L1/L2.
+// A CTA covers a 32 x 8 tile of the plane and marches through DH_Z planes:
+// per plane H_x (tile rows + x halo) and H_y (tile columns + y halo) are staged in
+// shared memory (the next plane's values are loaded into registers while the
+// current one is computed); H_z comes from a per-thread register window along z.
+constexpr int DH_Z = 8;
 template <int M>
-__global__ void __launch_bounds__(256) divh_kernel(const KParams p, double *__restrict__ qout,
-                                                   double *__restrict__ w,
-                                                   double *__restrict__ rout,
-                                                   unsigned int *__restrict__ flag, int zb,
-                                                   int ze) {
+struct DHGeom {
+  static constexpr int XW = 32 + 2 * M;                       // H_x row width
+  static constexpr int NX = 8 * XW, NY = (8 + 2 * M) * 32;    // staged elements
+  static constexpr int PER = (NX + NY + 255) / 256;           // per thread
+};
+template <int M, bool SYM>
+__device__ __forceinline__ void divh_fetch(const KParams &p, const double *__restrict__ H, int z,
+                                           int x0, int y0, int tid, double (&v)[DHGeom<M>::PER]) {
+  using G = DHGeom<M>;
   const size_t FS = (size_t)p.nx * p.ny;
-  const size_t n = (size_t)(ze - zb) * FS;
-  const double *H = p.hflux;
+  const double *hp = H + (size_t)z * 3 * FS;
+#pragma unroll
+  for (int r = 0; r < G::PER; ++r) {
+    const int idx = tid + 256 * r;
+    v[r] = 0.0;
+    if (idx < G::NX) {  // H_x: row ty, column c of the x-extended row
+      const int ty = idx / G::XW, c = idx - ty * G::XW;
+      int f;
+      const int gx = bmap_t<SYM>(x0 - M + c, p.nx, p.sym[0], f);
+      const int gy = min(y0 + ty, p.ny - 1);
+      const double h = __ldg(hp + (size_t)gy * p.nx + gx);
+      v[r] = f ? -h : h;
+    } else if (idx < G::NX + G::NY) {  // H_y: row c of the y-extended tile, column tx
+      const int j = idx - G::NX, c = j >> 5, tx = j & 31;
+      int f;
+      const int gy = bmap_t<SYM>(y0 - M + c, p.ny, p.sym[1], f);
+      const int gx = min(x0 + tx, p.nx - 1);
+      const double h = __ldg(hp + FS + (size_t)gy * p.nx + gx);
+      v[r] = f ? -h : h;
+    }
+  }
+}
+
+template <int M, bool SYM>
+__global__ void __launch_bounds__(256, 4) divh_kernel(const KParams p,
+                                                      const double *__restrict__ H,
+                                                      double *__restrict__ qout,
+                                                      double *__restrict__ w,
+                                                      double *__restrict__ rout,
+                                                      unsigned int *__restrict__ flag, int zb,
+                                                      int ze) {
+  using G = DHGeom<M>;
+  __shared__ double sh[G::NX + G::NY];
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
+  const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 8;
+  const int x = x0 + tx, y = y0 + ty;
+  const bool valid = x < p.nx && y < p.ny;
+  const int z0 = zb + blockIdx.z * DH_Z;
+  const int nzo = min(DH_Z, ze - z0);
+  const size_t FS = (size_t)p.nx * p.ny;
+  const size_t off = (size_t)min(y, p.ny - 1) * p.nx + min(x, p.nx - 1);
+  // register window of H_z along z
+  double hz[DH_Z + 2 * M];
+#pragma unroll
+  for (int t = 0; t < DH_Z + 2 * M; ++t) {
+    hz[t] = 0.0;
+    if (t < nzo + 2 * M) {
+      int f;
+      const int zz = zread(p, z0 - M + t, f);
+      const double v = __ldg(H + (size_t)zz * 3 * FS + 2 * FS + off);
+      hz[t] = f ? -v : v;
+    }
+  }
+  double nxt[G::PER];
+  divh_fetch<M, SYM>(p, H, z0, x0, y0, tid, nxt);
   bool bad = false;
-  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < n;
-       t += (size_t)gridDim.x * blockDim.x) {
-    const int z = zb + (int)(t / FS);
-    const size_t off = t % FS;
-    const int y = (int)(off / p.nx), x = (int)(off % p.nx);
-    const double *hx = H + (size_t)z * 3 * FS + (size_t)y * p.nx;
-    const double *hy = H + (size_t)z * 3 * FS + FS + x;
+#pragma unroll
+  for (int j = 0; j < DH_Z; ++j) {
+    if (j >= nzo) break;
+    const int z = z0 + j;
+    // this plane's read-modify-write operands, in flight during the staging below
+    const size_t o = (size_t)z * 5 * FS + 4 * FS + off;
+    double *qe = qout ? qout + qplane(p, z) + 4 * FS + off : nullptr;
+    double q_old = 0.0, w_old = 0.0;
+    if (valid && !rout) {
+      q_old = *qe;
+      if (p.write_w) w_old = w[o];
+    }
+    __syncthreads();  // the previous plane's reads are done
+#pragma unroll
+    for (int r = 0; r < G::PER; ++r) {
+      const int idx = tid + 256 * r;
+      if (idx < G::NX + G::NY) sh[idx] = nxt[r];
+    }
+    __syncthreads();
+    if (j + 1 < nzo) divh_fetch<M, SYM>(p, H, z + 1, x0, y0, tid, nxt);
+    const double *rx = sh + ty * G::XW + tx + M;
+    const double *cy = sh + G::NX + (ty + M) * 32 + tx;
     double sx = 0.0, sy = 0.0, sz = 0.0;
 #pragma unroll
     for (int k = 1; k <= M; ++k) {
-      int f1, f2;
-      const int xp = bmap(x + k, p.nx, p.sym[0], f1), xm = bmap(x - k, p.nx, p.sym[0], f2);
-      sx = fma(p.a[k - 1], (f1 ? -hx[xp] : hx[xp]) - (f2 ? -hx[xm] : hx[xm]), sx);
-      const int yp = bmap(y + k, p.ny, p.sym[1], f1), ym = bmap(y - k, p.ny, p.sym[1], f2);
-      sy = fma(p.a[k - 1],
-               (f1 ? -hy[(size_t)yp * p.nx] : hy[(size_t)yp * p.nx]) -
-                   (f2 ? -hy[(size_t)ym * p.nx] : hy[(size_t)ym * p.nx]),
-               sy);
-      const int zp = zread(p, z + k, f1), zm = zread(p, z - k, f2);
-      const double vp = H[(size_t)zp * 3 * FS + 2 * FS + off],
-                   vm = H[(size_t)zm * 3 * FS + 2 * FS + off];
-      sz = fma(p.a[k - 1], (f1 ? -vp : vp) - (f2 ? -vm : vm), sz);
+      sx = fma(p.a[k - 1], rx[k] - rx[-k], sx);
+      sy = fma(p.a[k - 1], cy[32 * k] - cy[-32 * k], sy);
+      sz = fma(p.a[k - 1], hz[j + M + k] - hz[j + M - k], sz);
     }
+    if (!valid) continue;
     const double d = sx + sy + sz;
-    const size_t o = (size_t)z * 5 * FS + 4 * FS + off;
     if (rout) {
       rout[o] += d;
       continue;
     }
     const double dd = p.dt * d;
-    double *qe = qout + qplane(p, z) + 4 * FS + off;
-    const double qn = fma(p.B, dd, *qe);
+    const double qn = fma(p.B, dd, q_old);
     *qe = qn;
     bad |= !isfinite(qn);
-    if (p.write_w) w[o] = fma(p.two_reg ? p.beta : 1.0, dd, w[o]);
+    if (p.write_w) w[o] = fma(p.two_reg ? p.beta : 1.0, dd, w_old);
   }
   if (bad) atomicOr(flag, 1u);
 }
@@ -411,10 +477,12 @@ cudaError_t launch_divh(const KParams &p, double *q_out, double *w, double *r_ou
                         unsigned int *flag, int zb, int ze, cudaStream_t s, long long *launches) {
   if (ze <= zb) return cudaSuccess;
   ++*launches;
-  const size_t n = (size_t)(ze - zb) * p.nx * p.ny;
-  size_t blocks = (n + 255) / 256;
-  if (blocks > 148 * 8) blocks = 148 * 8;
-#define DCALL(MM) divh_kernel<MM><<<(int)blocks, 256, 0, s>>>(p, q_out, w, r_out, flag, zb, ze)
+  const dim3 grid((p.nx + 31) / 32, (p.ny + 7) / 8, (ze - zb + DH_Z - 1) / DH_Z);
+  const dim3 block(32, 8);
+  const bool sym = p.sym[0] || p.sym[1];
+#define DCALL(MM)                                                                   \
+  if (sym) divh_kernel<MM, true><<<grid, block, 0, s>>>(p, p.hflux, q_out, w, r_out, flag, zb, ze); \
+  else divh_kernel<MM, false><<<grid, block, 0, s>>>(p, p.hflux, q_out, w, r_out, flag, zb, ze)
   switch (p.m) {
     case 1: DCALL(1); break;
     case 2: DCALL(2); break;
