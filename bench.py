@@ -30,6 +30,17 @@ CONFIGS = {
     "tgv256_o12": dict(n=256, order=12, scheme=1, desc="BASELINE configs[3]: TGV 256^3 12th order RK3"),
     "tgv256_o8": dict(n=256, order=8, scheme=1, desc="BASELINE configs[4]: TGV 256^3/GPU 8th order RK3"),
     "tgv64_o4": dict(n=64, order=4, scheme=1, desc="BASELINE configs[1]: TGV 64^3 4th order RK3"),
+    # SURVEY §8(f) N2-N4 variants of the headline workload (not the driver's default line)
+    "tgv256_o12_rk3_2r": dict(n=256, order=12, scheme=2,
+                              desc="N2(a): TGV 256^3 12th order, two-register RK3 (D-25)"),
+    "tgv256_o12_cons": dict(n=256, order=12, scheme=1, cons=True,
+                            desc="N2(b): TGV 256^3 12th order RK3, conservative viscous work (D-27)"),
+    "tgv256_o12_sutherland": dict(n=256, order=12, scheme=1, visc=True,
+                                  desc="N4: TGV 256^3 12th order RK3, Sutherland mu(T), "
+                                       "S/T_ref = 110.4/288 (D-26)"),
+    "tgv256_o12_sym": dict(n=256, order=12, scheme=1, sym=True,
+                           desc="N3: 256^3 12th order RK3 with symmetry boundaries in x, y, z "
+                                "(TGV state; timing of the mirrored-halo kernels)"),
     # the paper's scalar verification equation in 3D
     "scalar256_o12": dict(n=256, order=12, scheme=1, scalar=True,
                           desc="N1: scalar advection-diffusion 256^3, 12th order RK3, "
@@ -156,18 +167,31 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def oracle_rate(order: int, dx: float, dt: float, budget_s: float, min_steps: int = 1):
+SUTH = 110.4 / 288.0
+
+
+def oracle_params(cfg, n, dx, dt):
+    """OracleParams of a bench config (variants included) on an n^3 sample."""
+    from inputs import TGV_PHYS
+    from oracle import core
+    return core.OracleParams(n, n, n, cfg["order"], dx, dt=dt, energy_form=int(cfg.get("cons", 0)),
+                             visc_law=int(cfg.get("visc", 0)),
+                             suth=SUTH if cfg.get("visc") else 0.0,
+                             sym=(1, 1, 1) if cfg.get("sym") else (0, 0, 0), **TGV_PHYS)
+
+
+def oracle_rate(cfg, dx: float, dt: float, budget_s: float, min_steps: int = 1):
     """Oracle (single-threaded C++) RK3 throughput on a bounded sample: a periodic
     24^3 grid at the workload's spacing, order, time step and TGV state."""
-    from inputs import TGV_PHYS, tgv
+    from inputs import tgv
     from oracle import core
     n = 24
-    p = core.OracleParams(n, n, n, order, dx, dt=dt, **TGV_PHYS)
+    p = oracle_params(cfg, n, dx, dt)
     Q = tgv(n, n, n, dx=dx)
     t0 = time.perf_counter()
     steps = 0
     while steps < min_steps or time.perf_counter() - t0 < budget_s:
-        Q = core.step(p, Q, 1, 1)
+        Q = core.step(p, Q, cfg["scheme"], 1)
         steps += 1
     el = time.perf_counter() - t0
     return n ** 3 * steps / el, steps, el, f"oracle RK3 on a periodic 24^3 TGV sample at the workload's dx/order/dt, {steps} steps, {el:.1f} s"
@@ -192,9 +216,9 @@ def run_reference(args, cfg, n_glob, dx, dt):
         Q = np.sin(X) * np.cos(Y) * np.cos(Z)
         adv = lambda st, k: core.scalar_step(p, (1.0, -0.5, 0.25), 0.75, st, 1, k)  # noqa: E731
     else:
-        p = core.OracleParams(ns, ns, ns, cfg["order"], dx, dt=dt, **TGV_PHYS)
+        p = oracle_params(cfg, ns, dx, dt)
         Q = tgv(ns, ns, ns, dx=dx)
-        adv = lambda st, k: core.step(p, st, 1, k)  # noqa: E731
+        adv = lambda st, k: core.step(p, st, cfg["scheme"], k)  # noqa: E731
     for _ in range(args.warmup):
         Q = adv(Q, 1)
     t0 = time.perf_counter()
@@ -252,6 +276,13 @@ def main():
     nz_glob = n * world  # weak scaling: 256^3 per GPU, TGV periods tiled in z
     solver = osbli.Solver(n, n, nz_glob, cfg["order"], dx, dt, scheme=cfg["scheme"], rank=rank,
                           nranks=world, unique_id=uid, **TGV_PHYS)
+    if cfg.get("visc"):
+        solver.set_viscosity(osbli.OSBLI_VISC_SUTHERLAND, SUTH)
+    if cfg.get("cons"):
+        solver.set_energy_form(osbli.OSBLI_ENERGY_CONSERVATIVE)
+    if cfg.get("sym"):
+        for d in range(3 if world == 1 else 2):
+            solver.set_boundary(d, osbli.OSBLI_BC_SYMMETRY)
     stream = torch.cuda.Stream()
     solver.set_stream(stream.cuda_stream)
     # input: this rank's slab of the global TGV, generated on the host, copied in
@@ -360,6 +391,9 @@ def main():
         "algorithmic_bytes_per_launch": (xyb if dom == "xypass" else zb) / 3 * per_launch_pts,
         "peak_source": f"FP64 = 148 SMs x 64 lanes x 2 flop x {fmax:.0f} MHz (guide unit counts; DESIGN.md §5)",
         "flops_per_point": fl, "avg_launch_ms": avg,
+        "flops_model": ("default operator (DESIGN.md §5); the variant's extra terms are not "
+                        "counted, so frac is a lower bound") if any(
+                            cfg.get(k) for k in ("visc", "cons", "sym")) else "DESIGN.md §5",
         "share_of_step": (xyms if dom == "xypass" else zms) / ms if ms > 0 else None,
         "other_kernel": {"name": "zpass" if dom == "xypass" else "xypass",
                          "avg_launch_ms": z_avg if dom == "xypass" else xy_avg,
@@ -376,7 +410,9 @@ def main():
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": cfg["desc"], "grid": [n, n, nz_glob], "order": cfg["order"],
-                   "scheme": "rk3", "Re": 1600.0, "dt": dt,
+                   "scheme": {0: "euler", 1: "rk3", 2: "rk3-2r"}[cfg["scheme"]], "Re": 1600.0,
+                   "dt": dt,
+                   "variant": {k: cfg[k] for k in ("visc", "cons", "sym") if cfg.get(k)} or None,
                    "l2": "inputs larger than L2 (state 5 x 8 B x %d pts = %.0f MB per field-set)"
                    % (npts_local, state_bytes / 1e6),
                    "parallelism": f"z-slab x{world}"},
@@ -390,7 +426,7 @@ def main():
                 "d2h_bytes_per_step": state_bytes, "steps": args.e2e_steps},
     }
     if world == 1 and not args.no_cpu_baseline:
-        rate, steps, el, sample = oracle_rate(cfg["order"], dx, dt, budget_s=15.0)
+        rate, steps, el, sample = oracle_rate(cfg, dx, dt, budget_s=15.0)
         line["cpu_baseline"] = {"value": rate, "unit": "pt-steps/s", "cores": 1, "kind": "oracle",
                                 "sample": sample}
     print(json.dumps(line), flush=True)

@@ -47,6 +47,19 @@ __device__ __forceinline__ int bmap(int i, int n, int sym, int &flip) {
     flip = 0;
     return wrapi(i, n);
   }
+  // one reflection at most (every halo of a grid at least m points wide)
+  if ((unsigned)i < (unsigned)n) {
+    flip = 0;
+    return i;
+  }
+  if (i < 0 && i >= -n) {
+    flip = 1;
+    return -1 - i;
+  }
+  if (i >= n && i < 2 * n) {
+    flip = 1;
+    return 2 * n - 1 - i;
+  }
   int c = i % (2 * n);
   if (c < 0) c += 2 * n;
   flip = c >= n;

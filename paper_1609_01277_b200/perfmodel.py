@@ -25,16 +25,23 @@ COMPULSORY_BYTES_EULER = 80.0
 
 
 def kernel_bytes(stage: int, scheme: int = 1):
-    """(zpass_bytes, xypass_bytes) per point for RK3 stage 0/1/2 (Euler: stage 0, scheme 0)."""
-    read_w = scheme == 1 and stage > 0
-    write_w = scheme == 1 and stage < 2
+    """(zpass_bytes, xypass_bytes) per point for RK3 stage 0/1/2 (Euler: stage 0, scheme 0).
+
+    scheme 2 (two-register RK3): the z-pass never reads the register (it writes
+    dt Rz into the destination buffer), the xy-pass reads Q_old instead."""
+    read_w = scheme in (1, 2) and stage > 0
+    write_w = scheme in (1, 2) and stage < 2
+    if scheme == 2:
+        z = 40.0 + 40.0 + 24.0  # read Q; write dt Rz, g_i2
+        xy = 40.0 + 24.0 + 40.0 + (40.0 if read_w else 0.0) + 40.0 + (40.0 if write_w else 0.0)
+        return z, xy
     z = 40.0 + (40.0 if read_w else 0.0) + 40.0 + 24.0  # read Q (and W); write W', g_i2
     xy = 40.0 + 24.0 + 40.0 + 40.0 + (40.0 if write_w else 0.0)  # read Q, g, W'; write Q' (and W)
     return z, xy
 
 
 def step_kernel_bytes(scheme: int = 1):
-    st = 3 if scheme == 1 else 1
+    st = 1 if scheme == 0 else 3
     zs = sum(kernel_bytes(s, scheme)[0] for s in range(st))
     xs = sum(kernel_bytes(s, scheme)[1] for s in range(st))
     return zs, xs
