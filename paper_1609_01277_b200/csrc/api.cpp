@@ -165,6 +165,11 @@ int create_common(osbli_ctx *h) {
   osbli::central_weights(h->m, a, b);
   for (int k = 0; k < h->m; ++k) p.a[k] = a[k] / h->dx;
   for (int k = 0; k <= h->m; ++k) p.b[k] = b[k] / (h->dx * h->dx);
+  for (int l = 0; l < h->m; ++l) {
+    double c = 0.0;
+    for (int k = h->m; k > l; --k) c += b[k];
+    p.cb[l] = c / (h->dx * h->dx);
+  }
   const bool inviscid = std::isinf(h->Re);
   p.nu = inviscid ? 0.0 : 1.0 / h->Re;
   p.kappa = inviscid ? 0.0 : 1.0 / ((h->gamma - 1.0) * h->Minf * h->Minf * h->Pr * h->Re);

@@ -112,6 +112,10 @@ __device__ __forceinline__ double sutherland_dmu(const KParams &p, double T, dou
   return mu * (1.5 / T - 1.0 / (T + p.suth));
 }
 
+// second derivatives in first differences (D-22); 0 selects the (f+ + f-) - 2f form
+#ifndef OSBLI_D2_SBP
+#define OSBLI_D2_SBP 1
+#endif
 #include "zpass.cuh"
 #include "xypass.cuh"
 #include "xypass_ws.cuh"

@@ -15,6 +15,7 @@ struct KParams {
   int m;           // stencil half width
   double a[kMaxHalf];      // first-derivative weights a_k / dx       (k = 1..m)
   double b[kMaxHalf + 1];  // second-derivative weights b_k / dx^2    (k = 0..m)
+  double cb[kMaxHalf];     // C_l = sum_{k>l} b_k / dx^2 (l = 0..m-1): D2 in first differences
   double nu, kappa;        // 1/Re and 1/((gamma-1) M^2 Pr Re)  (mu = 1)
   double gm1;              // gamma - 1
   double gM2;              // gamma M^2

@@ -107,6 +107,18 @@ __device__ __forceinline__ double wd1(const KParams &p, const double (&v)[W], in
 // second derivative, exactly zero on a constant window: sum b_k ((f+ + f-) - 2 f)  (D-22)
 template <int M, int W>
 __device__ __forceinline__ double wd2(const KParams &p, const double (&v)[W], int j) {
+#if OSBLI_D2_SBP
+  // in first differences (summation by parts): sum_l C_l (d_{c+l} - d_{c-1-l}),
+  // d_i = v[i+1] - v[i] shared by the outputs of the window; exact zero on constants
+  double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+  for (int l = 0; l < M; ++l) {
+    const double t = (v[j + M + l + 1] - v[j + M + l]) - (v[j + M - l] - v[j + M - l - 1]);
+    if (l & 1) s1 = fma(p.cb[l], t, s1);
+    else s0 = fma(p.cb[l], t, s0);
+  }
+  return s0 + s1;
+#else
   const double c = v[j + M];
   double s0 = 0.0, s1 = 0.0;
 #pragma unroll
@@ -116,6 +128,7 @@ __device__ __forceinline__ double wd2(const KParams &p, const double (&v)[W], in
     else s1 = fma(p.b[k], t, s1);
   }
   return s0 + s1;
+#endif
 }
 
 // Velocity group, one direction (DIR 0 = x: phase X, DIR 1 = y: phase Y):

@@ -92,6 +92,16 @@ __device__ __forceinline__ double d1w(const KParams &p, const double (&v)[ZP_RZ 
 // exactly zero on a constant window (D-22)
 template <int M>
 __device__ __forceinline__ double d2w(const KParams &p, const double (&v)[ZP_RZ + 2 * M], int j) {
+#if OSBLI_D2_SBP
+  double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+  for (int l = 0; l < M; ++l) {
+    const double t = (v[j + M + l + 1] - v[j + M + l]) - (v[j + M - l] - v[j + M - l - 1]);
+    if (l & 1) s1 = fma(p.cb[l], t, s1);
+    else s0 = fma(p.cb[l], t, s0);
+  }
+  return s0 + s1;
+#else
   const double c = v[j + M];
   double s0 = 0.0, s1 = 0.0;
 #pragma unroll
@@ -101,6 +111,7 @@ __device__ __forceinline__ double d2w(const KParams &p, const double (&v)[ZP_RZ 
     else s1 = fma(p.b[k], t, s1);
   }
   return s0 + s1;
+#endif
 }
 
 // ZF = 0: periodic z / ghost planes; 1: symmetry in z (mirrored plane reads);
