@@ -112,6 +112,25 @@ __device__ __forceinline__ double sutherland_dmu(const KParams &p, double T, dou
   return mu * (1.5 / T - 1.0 / (T + p.suth));
 }
 
+// 1/rho without the IEEE division's special-case path: the hardware seed
+// (rcp.approx.ftz.f64) and two Newton steps, accurate to about 1 ulp for the
+// normal, positive densities of the method (not correctly rounded: round-off only)
+#ifndef OSBLI_FAST_RCP
+#define OSBLI_FAST_RCP 1
+#endif
+__device__ __forceinline__ double rcp_rho(double x) {
+#if OSBLI_FAST_RCP
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+#else
+  return 1.0 / x;
+#endif
+}
+
 // second derivatives in first differences (D-22); 0 selects the (f+ + f-) - 2f form
 #ifndef OSBLI_D2_SBP
 #define OSBLI_D2_SBP 1

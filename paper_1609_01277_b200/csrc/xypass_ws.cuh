@@ -397,7 +397,7 @@ __global__ void __launch_bounds__(XY_CTA, 1)
         const int s = hy * PX + hx;
         const double rho = Sb[XF_RHO * FSZ + s], m0 = Sb[XF_M0 * FSZ + s],
                      m1 = Sb[XF_M1 * FSZ + s], m2 = Sb[XF_M2 * FSZ + s], e = Sb[XF_E * FSZ + s];
-        const double r = 1.0 / rho;
+        const double r = rcp_rho(rho);
         PR[XP_P * FSZ + s] = p.gm1 * (e - 0.5 * r * (m0 * m0 + m1 * m1 + m2 * m2));
         PR[XP_R * FSZ + s] = r;
       }

@@ -42,7 +42,7 @@ template <int M>
 __device__ __forceinline__ void zstore(const KParams &p, double *S, int slot, int c, double rho,
                                        double m0, double m1, double m2, double e) {
   constexpr int NR = ZGeom<M>::NR;
-  const double r = 1.0 / rho;
+  const double r = rcp_rho(rho);
   const double u0 = m0 * r, u1 = m1 * r, u2 = m2 * r;
   const double pr = p.gm1 * (e - 0.5 * (m0 * u0 + m1 * u1 + m2 * u2));
   const double T = p.gM2 * pr * r;
