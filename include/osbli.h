@@ -150,6 +150,15 @@ int osbli_set_stream(osbli_ctx *h, void *cuda_stream);
 int osbli_set_state(osbli_ctx *h, const double *q, int on_device);
 int osbli_get_state(osbli_ctx *h, double *q, int on_device);
 
+/* Stream-ordered forms of the two copies: enqueued on the handle's stream and
+ * returned from at once (no synchronisation).  Host buffers should be pinned
+ * (page-locked), or the copy is not asynchronous; the caller keeps q alive and
+ * unchanged (set) or unread (get) until the stream has passed the copy
+ * (osbli_sync, or any event recorded after it).  Used to overlap the host
+ * copies of several handles with each other's steps. */
+int osbli_set_state_async(osbli_ctx *h, const double *q, int on_device);
+int osbli_get_state_async(osbli_ctx *h, double *q, int on_device);
+
 /* Advance n >= 0 full time steps (3 stages for RK3).  Stream-ordered. */
 int osbli_step(osbli_ctx *h, int n);
 

@@ -363,7 +363,7 @@ int osbli_set_stream(osbli_ctx *h, void *cuda_stream) {
   return OSBLI_OK;
 }
 
-int osbli_set_state(osbli_ctx *h, const double *q, int on_device) {
+static int set_state_impl(osbli_ctx *h, const double *q, int on_device, bool sync) {
   int u = check_usable(h);
   if (u) return u;
   if (!q) return fail(h, OSBLI_E_INVAL, "null state pointer");
@@ -375,20 +375,34 @@ int osbli_set_state(osbli_ctx *h, const double *q, int on_device) {
   CK(h, osbli::launch_abi_to_internal(h->base, stage, h->b.q[h->cur], h->stream, &h->launches));
   if (h->ev_qready) CK(h, cudaEventRecord(h->ev_qready, h->stream));
   CK(h, cudaMemsetAsync(h->b.flag, 0, sizeof(unsigned int), h->stream));
-  CK(h, cudaStreamSynchronize(h->stream));
+  if (sync) CK(h, cudaStreamSynchronize(h->stream));
   h->step_count = 0;
   return OSBLI_OK;
 }
 
-int osbli_get_state(osbli_ctx *h, double *q, int on_device) {
+static int get_state_impl(osbli_ctx *h, double *q, int on_device, bool sync) {
   if (!h || !q) return OSBLI_E_INVAL;
   const size_t n = (size_t)5 * h->nz * h->nx * h->ny;
   double *stage = h->b.q[h->cur ^ 1];  // idle ping-pong buffer as ABI-layout staging
   CK(h, osbli::launch_internal_to_abi(h->base, h->b.q[h->cur], stage, 5, 1, h->stream, &h->launches));
   CK(h, cudaMemcpyAsync(q, stage, n * sizeof(double),
                         on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, h->stream));
-  CK(h, cudaStreamSynchronize(h->stream));
+  if (sync) CK(h, cudaStreamSynchronize(h->stream));
   return OSBLI_OK;
+}
+
+int osbli_set_state(osbli_ctx *h, const double *q, int on_device) {
+  return set_state_impl(h, q, on_device, true);
+}
+int osbli_get_state(osbli_ctx *h, double *q, int on_device) {
+  return get_state_impl(h, q, on_device, true);
+}
+int osbli_set_state_async(osbli_ctx *h, const double *q, int on_device) {
+  return set_state_impl(h, q, on_device, false);
+}
+int osbli_get_state_async(osbli_ctx *h, double *q, int on_device) {
+  if (h && h->poisoned) return OSBLI_E_STATE;
+  return get_state_impl(h, q, on_device, false);
 }
 
 }  // extern "C"

@@ -88,6 +88,8 @@ def load():
     L.osbli_loopback_step.argtypes = [ctypes.POINTER(H), c_int, c_int]
     L.osbli_set_source.argtypes = [H, vp, c_int]
     L.osbli_set_boundary.argtypes = [H, c_int, c_int]
+    L.osbli_set_state_async.argtypes = [H, vp, c_int]
+    L.osbli_get_state_async.argtypes = [H, vp, c_int]
     L.osbli_set_viscosity.argtypes = [H, c_int, ctypes.c_double]
     L.osbli_set_energy_form.argtypes = [H, c_int]
     L.osbli_scalar_create.argtypes = [c_int, c_int, c_int, c_int, c_double, c_double, c_double,
@@ -207,6 +209,21 @@ class Solver:
             out = np.empty(self.shape, dtype=np.float64)
         p, dev = _ptr(out)
         self._check(self._L.osbli_get_state(self._h, ctypes.c_void_p(p), dev))
+        return out
+
+    def set_state_async(self, q):
+        """Stream-ordered set_state (q: pinned host or device tensor, kept alive by the caller)."""
+        if tuple(q.shape) != self.shape:
+            raise ValueError(f"state shape {tuple(q.shape)} != {self.shape}")
+        p, dev = _ptr(q)
+        self._check(self._L.osbli_set_state_async(self._h, ctypes.c_void_p(p), dev))
+
+    def get_state_async(self, out):
+        """Stream-ordered get_state into out (pinned host or device tensor)."""
+        if tuple(out.shape) != self.shape:
+            raise ValueError(f"state shape {tuple(out.shape)} != {self.shape}")
+        p, dev = _ptr(out)
+        self._check(self._L.osbli_get_state_async(self._h, ctypes.c_void_p(p), dev))
         return out
 
     def step(self, n: int = 1):

@@ -299,3 +299,32 @@ def test_kernels_are_deterministic(osbli, order, shape):
     s.set_state(Q)
     s.step(2)
     assert np.array_equal(s.get_state(), Q2)
+
+
+def test_async_state_io_overlapped_handles(osbli, orc):
+    """osbli_set_state_async / osbli_get_state_async: three handles on their own
+    streams, each step's input copied in from pinned host memory and its result
+    copied out, all enqueued before one synchronisation — the results equal the
+    oracle's step (the pattern bench.py's e2e line times)."""
+    import torch
+    shape, order = (24, 20, 18), 8
+    dx, dt = 2 * math.pi / 24, 2e-3
+    Qs = [perturbed_tgv(*shape, dx=dx, amp=0.02, seed=100 + k) for k in range(3)]
+    qh = [torch.from_numpy(q).pin_memory() for q in Qs]
+    qo = [torch.empty_like(q).pin_memory() for q in qh]
+    solvers, streams = [], []
+    for k in range(3):
+        s = make(osbli, shape, order, dx, dt)
+        st = torch.cuda.Stream()
+        s.set_stream(st.cuda_stream)
+        solvers.append(s)
+        streams.append(st)
+    for k in range(3):
+        solvers[k].set_state_async(qh[k])
+        solvers[k].step(1)
+        solvers[k].get_state_async(qo[k])
+    torch.cuda.synchronize()
+    for k in range(3):
+        solvers[k].sync()
+        ref = orc.step(orc.OracleParams(*shape, order, dx, dt=dt, **TGV_PHYS), Qs[k], 1, 1)
+        assert np.all(relerr(qo[k].numpy(), ref) < TOL)
