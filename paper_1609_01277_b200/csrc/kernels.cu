@@ -433,6 +433,8 @@ cudaError_t xypass_launch(const KParams &p, const double *q, double *qout, doubl
             (ze - zb + seg - 1) / seg);
   kern<<<grid, ws::XY_CTA, smem, s>>>(p, q, qout, w, gz, rout, flag, zb, ze, seg);
 #else
+  // the non-specialised comparison kernel has no equation variants
+  if (p.visc || p.cons) return cudaErrorNotSupported;
   constexpr int smem = xy_smem_bytes<M>();
   static bool init = false;
   if (!init) {

@@ -34,6 +34,15 @@ constexpr int XY_THREADS = 256;          // consumer threads
 #endif
 constexpr int XY_PROD = 32 * OSBLI_XY_PRODUCERS;  // producer threads
 constexpr int XY_CTA = XY_THREADS + XY_PROD;
+// register split (setmaxnreg): 128 producer threads x PROD + 256 consumers x CONS <= 64K
+#ifndef OSBLI_XY_PROD_REGS
+#define OSBLI_XY_PROD_REGS 40
+#endif
+#ifndef OSBLI_XY_CONS_REGS
+#define OSBLI_XY_CONS_REGS 232
+#endif
+constexpr int XY_PROD_REGS = OSBLI_XY_PROD_REGS;
+constexpr int XY_CONS_REGS = OSBLI_XY_CONS_REGS;
 // named barriers: 2 + b = buffer b full (producers -> group A); 4 + b = buffer b
 // empty (consumers -> producers); 7 = producers only; 1, 6, 8, 9, 10: consumers
 // (see the consumer loop)
@@ -358,7 +367,7 @@ __global__ void __launch_bounds__(XY_CTA, 1)
     // ---- producer warpgroup: plane i into buffer i & 1 once the consumers released it;
     //      it needs few registers and hands the rest to the consumer warpgroups
 #if OSBLI_XY_PRODUCERS == 4
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(XY_PROD_REGS) : "memory");
 #endif
     const int lane = tid - XY_THREADS;
     for (int i = 0; i < nplanes; ++i) {
@@ -378,7 +387,7 @@ __global__ void __launch_bounds__(XY_CTA, 1)
   }
 
 #if OSBLI_XY_PRODUCERS == 4
-  asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(XY_CONS_REGS) : "memory");
 #endif
   // The two consumer groups run decoupled, one plane apart at most; they meet only
   // where data passes between them (named barriers, arrive -> sync):
