@@ -170,6 +170,19 @@ class ClockSampler:
 SUTH = 110.4 / 288.0
 
 
+def host_cpu():
+    """CPU model and logical CPU count of the host the oracle runs on."""
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"model": model, "nproc": os.cpu_count()}
+
+
 def oracle_params(cfg, n, dx, dt):
     """OracleParams of a bench config (variants included) on an n^3 sample."""
     from inputs import TGV_PHYS
@@ -235,6 +248,7 @@ def run_reference(args, cfg, n_glob, dx, dt):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": cfg["desc"], "grid": [n_glob] * 3, "order": cfg["order"]},
         "cpu_baseline": {"value": rate, "unit": "pt-steps/s", "cores": 1, "kind": "oracle",
+                         "host": host_cpu(),
                          "sample": sample},
         "e2e": {"value": rate, "unit": "pt-steps/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -468,6 +482,7 @@ def main():
     if world == 1 and not args.no_cpu_baseline:
         rate, steps, el, sample = oracle_rate(cfg, dx, dt, budget_s=15.0)
         line["cpu_baseline"] = {"value": rate, "unit": "pt-steps/s", "cores": 1, "kind": "oracle",
+                                "host": host_cpu(),
                                 "sample": sample}
     print(json.dumps(line), flush=True)
 
