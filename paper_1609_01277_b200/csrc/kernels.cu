@@ -103,15 +103,6 @@ __device__ __forceinline__ void cp_async8(double *smem, const double *gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
 }
 
-// Sutherland's law in dimensionless form (D-26): mu(T) = T^1.5 (1 + S)/(T + S),
-// mu(1) = 1, and its derivative mu'(T) = mu (3/(2T) - 1/(T + S))
-__device__ __forceinline__ double sutherland_mu(const KParams &p, double T) {
-  return T * sqrt(T) * (1.0 + p.suth) / (T + p.suth);
-}
-__device__ __forceinline__ double sutherland_dmu(const KParams &p, double T, double mu) {
-  return mu * (1.5 / T - 1.0 / (T + p.suth));
-}
-
 // 1/rho without the IEEE division's special-case path: the hardware seed
 // (rcp.approx.ftz.f64) and two Newton steps, accurate to about 1 ulp for the
 // normal, positive densities of the method (not correctly rounded: round-off only)
@@ -129,6 +120,24 @@ __device__ __forceinline__ double rcp_rho(double x) {
 #else
   return 1.0 / x;
 #endif
+}
+
+// Sutherland's law in dimensionless form (D-26): mu(T) = T^1.5 (1 + S)/(T + S),
+// mu(1) = 1, and its derivative mu'(T) = mu (3/(2T) - 1/(T + S))
+// (T^1.5 = T^2 / sqrt(T) from the hardware reciprocal-square-root seed and two
+// Newton steps; reciprocals as rcp_rho: about 1 ulp, round-off only, D-28)
+__device__ __forceinline__ double rsqrt_fast(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double hx = 0.5 * x;
+  y = y * fma(-hx * y, y, 1.5);
+  return y * fma(-hx * y, y, 1.5);
+}
+__device__ __forceinline__ double sutherland_mu(const KParams &p, double T) {
+  return (T * T) * rsqrt_fast(T) * ((1.0 + p.suth) * rcp_rho(T + p.suth));
+}
+__device__ __forceinline__ double sutherland_dmu(const KParams &p, double T, double mu) {
+  return mu * (1.5 * rcp_rho(T) - rcp_rho(T + p.suth));
 }
 
 // second derivatives in first differences (D-22); 0 selects the (f+ + f-) - 2f form
