@@ -650,33 +650,53 @@ __global__ void __launch_bounds__(XY_CTA, 1)
         // ---- epilogue: W <- W' + dt R_xy ; Q' <- Q + B W  (rows of 32 columns; residual
         //      mode: dt = 1, A = 0 so that W' = Rz and R = W' + R_xy)
         const int fidx[5] = {XF_RHO, XF_M0, XF_M1, XF_M2, XF_E};
+        // W' + dt R_xy of the four points first; then one uniform branch on the mode
+        double wn[5][4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int pt = (seg * XY_RY + j) * TP + col;
+#pragma unroll
+          for (int f = 0; f < 5; ++f)
+            wn[f][j] = fma(p.dt, XA[f * NPT + pt] + (XB[f * NPT + pt] + R[f][j]), wp[f][j]);
+        }
+        const int mode = rout ? 0 : (TR ? 3 : (p.write_w ? 1 : 2));
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const int ty = seg * XY_RY + j;
           const int y = y0 + ty;
           if (!xin || y >= p.ny) continue;
-          const int pt = ty * TP + col;
           const int c = (ty + M) * PX + col + M;
           const size_t o = (size_t)z * 5 * FS + (size_t)y * p.nx + x;
-          double *qo = qout ? qout + qplane(p, z) + (size_t)y * p.nx + x : nullptr;
+          if (mode == 0) {
 #pragma unroll
-          for (int f = 0; f < 5; ++f) {
-            const double rxy = XA[f * NPT + pt] + (XB[f * NPT + pt] + R[f][j]);
-            const double wn = fma(p.dt, rxy, wp[f][j]);
-            if (rout) {
-              rout[o + f * FS] = wn;
-              continue;
+            for (int f = 0; f < 5; ++f) rout[o + f * FS] = wn[f][j];
+            continue;
+          }
+          double *qo = qout + qplane(p, z) + (size_t)y * p.nx + x;
+          if (mode == 1) {  // 2N RK3 stages 1, 2: W <- W', Q' = Q + B W
+#pragma unroll
+            for (int f = 0; f < 5; ++f) {
+              w[o + f * FS] = wn[f][j];
+              const double qn = fma(p.B, wn[f][j], S[fidx[f] * FSZ + c]);
+              qo[f * FS] = qn;
+              bad |= !isfinite(qn);
             }
-            double qb = S[fidx[f] * FSZ + c];
-            if (TR) {  // w holds Q_old
-              if (p.read_w) qb = qold[f][j];
-              if (p.write_w) w[o + f * FS] = fma(p.beta, wn, qb);
-            } else if (p.write_w) {
-              w[o + f * FS] = wn;
+          } else if (mode == 2) {  // last stage / Euler: Q' = Q + B W
+#pragma unroll
+            for (int f = 0; f < 5; ++f) {
+              const double qn = fma(p.B, wn[f][j], S[fidx[f] * FSZ + c]);
+              qo[f * FS] = qn;
+              bad |= !isfinite(qn);
             }
-            const double qn = fma(p.B, wn, qb);
-            qo[f * FS] = qn;
-            bad |= !isfinite(qn);
+          } else {  // two-register RK3: w holds Q_old
+#pragma unroll
+            for (int f = 0; f < 5; ++f) {
+              const double qb = p.read_w ? qold[f][j] : S[fidx[f] * FSZ + c];
+              if (p.write_w) w[o + f * FS] = fma(p.beta, wn[f][j], qb);
+              const double qn = fma(p.B, wn[f][j], qb);
+              qo[f * FS] = qn;
+              bad |= !isfinite(qn);
+            }
           }
         }
         if (i + 1 < nplanes) nbar_arrive(10, XY_THREADS);  // done with XA
