@@ -437,7 +437,10 @@ cudaError_t xypass_launch(const KParams &p, const double *q, double *qout, doubl
     if (e != cudaSuccess) return e;
     init[v] = true;
   }
-  const int seg = ze - zb < ws::XY_SEG ? ze - zb : ws::XY_SEG;
+  // planes per CTA: XY_SEG, halved while the grid would not cover the SMs (small grids)
+  const int tiles = ((p.nx + ws::XY_TX - 1) / ws::XY_TX) * ((p.ny + ws::XY_TY - 1) / ws::XY_TY);
+  int seg = ze - zb < ws::XY_SEG ? ze - zb : ws::XY_SEG;
+  while (seg > 1 && tiles * ((ze - zb + seg - 1) / seg) < 148) seg = (seg + 1) / 2;
   dim3 grid((p.nx + ws::XY_TX - 1) / ws::XY_TX, (p.ny + ws::XY_TY - 1) / ws::XY_TY,
             (ze - zb + seg - 1) / seg);
   kern<<<grid, ws::XY_CTA, smem, s>>>(p, q, qout, w, gz, rout, flag, zb, ze, seg);
