@@ -29,6 +29,9 @@ sys.path.insert(0, ROOT)
 CONFIGS = {
     "tgv256_o12": dict(n=256, order=12, scheme=1, desc="BASELINE configs[3]: TGV 256^3 12th order RK3"),
     "tgv256_o8": dict(n=256, order=8, scheme=1, desc="BASELINE configs[4]: TGV 256^3/GPU 8th order RK3"),
+    "tgv256_o12_strong": dict(n=256, order=12, scheme=1, strong=True,
+                              desc="BASELINE configs[3]: TGV 256^3 12th order RK3, strong scaling "
+                                   "(one 256^3 box split into z-slabs)"),
     "tgv64_o4": dict(n=64, order=4, scheme=1, desc="BASELINE configs[1]: TGV 64^3 4th order RK3"),
     # SURVEY §8(f) N2-N4 variants of the headline workload (not the driver's default line)
     "tgv256_o12_rk3_2r": dict(n=256, order=12, scheme=2,
@@ -287,7 +290,9 @@ def main():
 
     rank, world, local, uid = osbli.init_distributed()
     torch.cuda.set_device(local)
-    nz_glob = n * world  # weak scaling: 256^3 per GPU, TGV periods tiled in z
+    # weak scaling (default): 256^3 per GPU, TGV periods tiled in z; strong: one
+    # 256^3 box split into z-slabs (BASELINE configs[3])
+    nz_glob = n if cfg.get("strong") else n * world
     solver = osbli.Solver(n, n, nz_glob, cfg["order"], dx, dt, scheme=cfg["scheme"], rank=rank,
                           nranks=world, unique_id=uid, **TGV_PHYS)
     if cfg.get("visc"):
@@ -458,7 +463,8 @@ def main():
     line = {
         "metric": "grid-point RK3 updates/s (fp64)", "value": value, "unit": "pt-steps/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong" if cfg.get("strong") else "weak",
+        "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": cfg["desc"], "grid": [n, n, nz_glob], "order": cfg["order"],
                    "scheme": {0: "euler", 1: "rk3", 2: "rk3-2r"}[cfg["scheme"]], "Re": 1600.0,
