@@ -9,12 +9,18 @@
 //            operands in shared memory (computed once per staged point) and
 //            each thread produces RZ = 4 consecutive z outputs from a register
 //            window (reuse (RZ+2m)/RZ instead of 2m loads per output).
-//   xypass : all x/y terms on a 32x8 plane tile with an m-wide halo in
-//            shared memory, the mixed derivatives (commuted so that no z
-//            stencil is needed: D_x D_z u_z = D_x g_22, D_z D_x u_x = D_x g_02,
-//            ...; D-7), the viscous dissipation and heat flux, then
-//            the fused low-storage RK stage update W <- A W + dt R,
-//            Q' <- Q + B W and a non-finite check.
+//   xypass : all x/y terms on a 32x16 plane tile with an m-wide halo in
+//            shared memory (warp-specialised: a cp.async producer warpgroup and
+//            two decoupled consumer groups, xypass_ws.cuh), the mixed
+//            derivatives (commuted so that no z stencil is needed:
+//            D_x D_z u_z = D_x g_22, D_z D_x u_x = D_x g_02, ...; D-7),
+//            the viscous dissipation and heat flux, then the fused low-storage
+//            RK stage update W <- W' + dt R_xy, Q' <- Q + B W and
+//            a non-finite check.
+//   variants: symmetry boundaries (mirror maps, N3), the
+//            two-register RK3 (N2a), Sutherland mu(T) and the conservative
+//            viscous work (+ divh_kernel; N2b, N4), each a separate
+//            instantiation so that the default path stays as it is.
 // All arithmetic is IEEE fp64; tensor cores are not used (a stencil is not a
 // dense contraction).  Periodic wrap in x and y is done in-kernel; in
 // z either in-kernel (one GPU) or through ghost planes (slab decomposition).

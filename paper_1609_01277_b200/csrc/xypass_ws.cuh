@@ -2,28 +2,26 @@ namespace ws {
 // xy-pass (included by kernels.cu inside namespace osbli::{anon}).
 //
 // A CTA owns a 32 x 16 tile of the xy-plane and marches through a segment of
-// z-planes (persistent, one CTA per SM), warp-specialised: warps 0-7 compute,
-// warps 8-11 are producers that stream the next plane into the other plane buffer
-// with cp.async while the consumers work on the current one (full/empty
-// handshake on named barriers), so the consumer warps spend no issue slots and
-// no registers on staging.  Per plane, shared memory
-// holds on the tile plus an m-wide halo (periodic wrap in x, y):
-//   rho, m0, m1, m2, e, g22  (double-buffered plane buffers, filled by cp.async)
-//   g02 on the tile rows (x-halo), g12 on the tile columns (y-halo)  (same buffers)
-//   p, r = 1/rho  (formulas P:127; EOS P:259-266; computed once per point)
-// (g_i2 = D_z u_i come from the z-pass).  u_i = m_i r and T = gamma M^2 p r are
-// formed on the fly in register windows.  While plane z is computed, plane
-// z+1 streams into the other plane buffer (cp.async) and its low-storage
-// register W' (= A W + dt Rz from the z-pass) into L2, so HBM latency hides
-// behind the FP64 work.  Each thread evaluates derivatives from register windows of RX = RY = 4
-// consecutive outputs ((4 + 2m) shared loads for 4 outputs), and the 8 warps
-// split into a velocity group (A: velocity gradients, viscous Laplacians,
-// mixed derivatives, heat flux, dissipation) and a conservative group (B:
-// skew-symmetric advection and fluxes).
-//   phase X  : x-derivatives of tile rows (A, B) + g00, g10 on the halo rows (ext)
-//   phase Y  : y-derivatives (A, B), combined with phase-X partials; group B
-//              then completes the stage for its points:
-//              W <- W' + dt (A + B), Q' <- Q + B W  (low-storage RK)
+// z-planes (one CTA per SM), warp-specialised:
+//   producers (warps 8-11, setmaxnreg 40): stream plane z+1 into the other plane
+//     buffer with cp.async (periodic wrap or mirror in x, y) and prefetch its
+//     low-storage register W' (= A W + dt Rz from the z-pass) into L2;
+//   group A (velocity, 4 warps, setmaxnreg 232): p and 1/rho of every staged
+//     point (formulas P:127, EOS P:259-266), velocity gradients, viscous
+//     Laplacians, mixed derivatives (commuted: D-7), dissipation;
+//   group B (conservative, 4 warps): skew-symmetric advection and fluxes
+//     (P:271-274), heat flux, and the stage update of its points,
+//     W <- W' + dt R_xy, Q' <- Q + B W.
+// Per plane, shared memory holds on the tile plus an m-wide halo: rho, m_i, e,
+// g22 (double-buffered plane buffers), g02 on the tile rows (x-halo), g12 on
+// the tile columns (y-halo); p, 1/rho; g00, g10 extended over the y-halo; the
+// groups' x-partials XA, XB.  u_i = m_i r and T = gamma M^2 p r are formed in
+// register windows of RX = RY = 4 consecutive outputs ((4 + 2m) shared loads
+// for 4 outputs).  Per plane: phase X (thread = 4-wide row segment) and phase Y
+// (thread = 4-tall column segment) in each group.  The groups run decoupled, up
+// to a plane apart, meeting only where data passes (named barriers, see the
+// consumer loop); group A computes the next plane's p, 1/rho while group B
+// finishes its epilogue.
 constexpr int XY_TX = 32;
 constexpr int XY_TY = 16;
 constexpr int XY_RX = 4;
