@@ -24,7 +24,7 @@ from . import core
 def sample_step(p: core.OracleParams, Q: np.ndarray, points, scheme: int, nsteps: int):
     """Return the oracle's Q after `nsteps` at each (i, j, k) in `points` -> [len, 5]."""
     m = p.order // 2
-    S = nsteps * (3 if scheme == 1 else 1)
+    S = nsteps * (1 if scheme == 0 else 3)
     h = S * m
     Q = np.asarray(Q).reshape(p.shape)
     out = np.zeros((len(points), 5))

@@ -328,3 +328,30 @@ def test_async_state_io_overlapped_handles(osbli, orc):
         solvers[k].sync()
         ref = orc.step(orc.OracleParams(*shape, order, dx, dt=dt, **TGV_PHYS), Qs[k], 1, 1)
         assert np.all(relerr(qo[k].numpy(), ref) < TOL)
+
+
+def test_large_grid_64bit_offsets(osbli, orc):
+    """The largest per-GPU box of the weak-scaling series (BASELINE configs[4]:
+    1024x512x512 on 8 GPUs = 512x512x256 per GPU), 8th order, one RK3 step: byte
+    offsets beyond 2^31 in every buffer.  Sampled points (corners, tile and plane
+    edges, the far end) against the windowed oracle; mass conserved."""
+    import psutil
+    from oracle import windowed
+    nx, ny, nz, order = 512, 512, 256, 8
+    if psutil.virtual_memory().available < 24e9:
+        pytest.skip("needs ~24 GB of host memory for the 512x512x256 state")
+    dx = 2 * math.pi / 256
+    dt = tgv_dt(256)
+    Q = tgv(nx, ny, nz, dx=dx)
+    s = make(osbli, (nx, ny, nz), order, dx, dt)
+    s.set_state(Q)
+    s.step(1)
+    Qg = s.get_state()
+    pts = [(0, 0, 0), (nx - 1, ny - 1, nz - 1), (31, 15, 7), (32, 16, 8), (nx // 2, ny - 1, 0),
+           (nx - 1, 0, nz // 2), (257, 300, 129), (100, 511, 255)]
+    p = orc.OracleParams(nx, ny, nz, order, dx, dt=dt, **TGV_PHYS)
+    So = windowed.sample_step(p, Q, pts, 1, 1)
+    scale = np.max(np.abs(Qg.reshape(5, -1)), axis=1)
+    for t, (i, j, k) in enumerate(pts):
+        assert np.all(np.abs(Qg[:, k, j, i] - So[t]) / scale < TOL), (i, j, k)
+    assert abs(Qg[0].sum() - Q[0].sum()) / Q[0].sum() < 1e-13
