@@ -261,6 +261,7 @@ __device__ __forceinline__ void xy_issue_plane(const KParams &p, const double *_
   const size_t FS = (size_t)p.nx * p.ny;
   const double *qp = q + qplane(p, z);
   const double *gp = gz + (size_t)z * 3 * FS;
+#pragma unroll 1
   for (int idx = tid; idx < HY * HX; idx += nthr) {
     const int hy = idx / HX, hx = idx - hy * HX;
     int fx, fy;
@@ -271,6 +272,7 @@ __device__ __forceinline__ void xy_issue_plane(const KParams &p, const double *_
     for (int f = 0; f < 5; ++f) cp_async8(d + f * FSZ, qp + f * FS + off);
     cp_async8(d + XF_G22 * FSZ, gp + 2 * FS + off);
   }
+#pragma unroll 1
   for (int idx = tid; idx < XY_TY * HX; idx += nthr) {
     const int ty = idx / HX, hx = idx - ty * HX;
     int fx, fy;
@@ -278,6 +280,7 @@ __device__ __forceinline__ void xy_issue_plane(const KParams &p, const double *_
                        bmap_t<SYM>(x0 - M + hx, p.nx, p.sym[0], fx);
     cp_async8(PB + Gm::PB_G02 + ty * PX + hx, gp + off);
   }
+#pragma unroll 1
   for (int idx = tid; idx < HY * XY_TX; idx += nthr) {
     const int hy = idx >> 5, tx = idx & 31;
     int fx, fy;
@@ -299,6 +302,7 @@ __device__ __forceinline__ void xy_mirror_signs(const KParams &p, double *PB, in
   const bool xs = p.sym[0] && (x0 - M < 0 || x0 + XY_TX + M > p.nx);
   const bool ys = p.sym[1] && (y0 - M < 0 || y0 + XY_TY + M > p.ny);
   if (!xs && !ys) return;
+#pragma unroll 1
   for (int idx = tid; idx < HY * HX; idx += nthr) {
     const int hy = idx / HX, hx = idx - hy * HX;
     int fx, fy;
@@ -316,6 +320,7 @@ __device__ __forceinline__ void xy_mirror_signs(const KParams &p, double *PB, in
 __device__ __forceinline__ void xy_prefetch_epilogue(const KParams &p, const double *w, int z,
                                                      int x0, int y0, int tid, int nthr) {
   const size_t FS = (size_t)p.nx * p.ny;
+#pragma unroll 1
   for (int t = tid; t < XY_TY * 5 * 2; t += nthr) {
     const int half = t & 1, a = (t >> 1) % 5, ty = (t >> 1) / 5;
     const int y = y0 + ty, x = min(x0 + 16 * half, p.nx - 1);
