@@ -404,6 +404,7 @@ __global__ void __launch_bounds__(XY_CTA, 1)
   if (grp == 0) {
     // formulas p and 1/rho once per point of a landed plane buffer
     auto formulas = [&](const double *Sb) {
+#pragma unroll 1
       for (int idx = q7; idx < HY * HX; idx += 128) {
         const int hy = idx / HX, hx = idx - hy * HX;
         const int s = hy * PX + hx;
