@@ -416,7 +416,7 @@ cudaError_t zpass_launch(const KParams &p, const double *q, double *w, double *g
   nseg = nseg < 1 ? 1 : (nseg > chunks ? chunks : nseg);
   const int seg_len = ((chunks + nseg - 1) / nseg) * ZP_TZ;
   nseg = (ze - zb + seg_len - 1) / seg_len;
-  dim3 grid(gx, gy, nseg);
+  dim3 grid(gx * gy, 1, nseg);
   kern<<<grid, ZP_THREADS, smem, s>>>(p, q, w, gz, zb, ze, seg_len);
   return cudaGetLastError();
 }

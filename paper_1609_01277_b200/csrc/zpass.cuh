@@ -128,7 +128,9 @@ __global__ void __launch_bounds__(ZP_THREADS, 1)
   extern __shared__ double S[];
   double *RB = S + Zg::RING;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int x0 = blockIdx.x * ZP_TX, y = blockIdx.y;
+  // blockIdx.x enumerates (x-tile, y-row) pencils (grid.y would cap ny at 65535)
+  const int gx = (p.nx + ZP_TX - 1) / ZP_TX;
+  const int x0 = (int)(blockIdx.x % gx) * ZP_TX, y = (int)(blockIdx.x / gx);
   const int zs = z_begin + blockIdx.z * seg_len;
   const int ze = min(z_end, zs + seg_len);
   if (zs >= ze) return;

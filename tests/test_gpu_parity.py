@@ -355,3 +355,16 @@ def test_large_grid_64bit_offsets(osbli, orc):
     for t, (i, j, k) in enumerate(pts):
         assert np.all(np.abs(Qg[:, k, j, i] - So[t]) / scale < TOL), (i, j, k)
     assert abs(Qg[0].sum() - Q[0].sum()) / Q[0].sum() < 1e-13
+
+
+@pytest.mark.parametrize("shape,direction", [((1, 70000, 1), 1), ((70000, 1, 2), 0)])
+def test_long_one_dimensional_grids(osbli, orc, shape, direction):
+    """Grids longer than 65535 points in y (and in x): every launch dimension holds."""
+    order, dx, dt = 4, 1e-3, 1e-5
+    Q = entropy_wave(*shape, dx=dx, A=0.2, k=3, U=0.4, Minf=1.0, direction=direction)
+    phys = dict(Re=math.inf, Pr=0.71, Minf=1.0, gamma=1.4)
+    s = make(osbli, shape, order, dx, dt, **phys)
+    s.set_state(Q)
+    s.step(2)
+    Qo = orc.step(orc.OracleParams(*shape, order, dx, dt=dt, **phys), Q, 1, 2)
+    assert np.all(relerr(s.get_state(), Qo) < TOL)
