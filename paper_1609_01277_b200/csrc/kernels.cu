@@ -396,6 +396,21 @@ __global__ void internal_to_abi_kernel(const KParams p, const double *__restrict
   }
 }
 
+// cudaFuncSetAttribute (dynamic shared memory above 48 KB) once per kernel and
+// device: `done` holds one bit per device id (handles on several devices may
+// share a process; a lost race only repeats the call)
+template <typename K>
+cudaError_t ensure_smem_attr(K kern, int smem, unsigned &done) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const unsigned bit = 1u << (dev & 31);
+  if (done & bit) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e == cudaSuccess) done |= bit;
+  return e;
+}
+
 template <int M>
 cudaError_t zpass_launch(const KParams &p, const double *q, double *w, double *gz, int zb, int ze,
                          cudaStream_t s) {
@@ -403,12 +418,9 @@ cudaError_t zpass_launch(const KParams &p, const double *q, double *w, double *g
   // symmetry in z (one GPU only) gets its own instantiation: mirrored plane reads
   const int sz = (p.visc || p.cons) ? 2 : (p.zwrap && p.sym[2] ? 1 : 0);
   auto kern = sz == 2 ? zpass_kernel<M, 2> : sz == 1 ? zpass_kernel<M, 1> : zpass_kernel<M, 0>;
-  static bool init[3] = {false, false, false};
-  if (!init[sz]) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    init[sz] = true;
-  }
+  static unsigned done[3] = {0, 0, 0};
+  cudaError_t e = ensure_smem_attr(kern, smem, done[sz]);
+  if (e != cudaSuccess) return e;
   const int gx = (p.nx + ZP_TX - 1) / ZP_TX, gy = p.ny;
   const int chunks = (ze - zb + ZP_TZ - 1) / ZP_TZ;
   // split the z-range into segments only when the pencils alone do not fill ~2 waves
@@ -436,13 +448,9 @@ cudaError_t xypass_launch(const KParams &p, const double *q, double *qout, doubl
               : v == 2 ? ws::xypass_kernel<M, 2>
               : v == 3 ? ws::xypass_kernel<M, 3>
                        : ws::xypass_kernel<M, 4>;
-  static bool init[5] = {false, false, false, false, false};
-  if (!init[v]) {
-    cudaError_t e =
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    init[v] = true;
-  }
+  static unsigned done[5] = {0, 0, 0, 0, 0};
+  cudaError_t e = ensure_smem_attr(kern, smem, done[v]);
+  if (e != cudaSuccess) return e;
   // planes per CTA: XY_SEG, halved while the grid would not cover the SMs (small grids)
   const int tiles = ((p.nx + ws::XY_TX - 1) / ws::XY_TX) * ((p.ny + ws::XY_TY - 1) / ws::XY_TY);
   int seg = ze - zb < ws::XY_SEG ? ze - zb : ws::XY_SEG;
@@ -454,13 +462,9 @@ cudaError_t xypass_launch(const KParams &p, const double *q, double *qout, doubl
   // the non-specialised comparison kernel has no equation variants
   if (p.visc || p.cons) return cudaErrorNotSupported;
   constexpr int smem = xy_smem_bytes<M>();
-  static bool init = false;
-  if (!init) {
-    cudaError_t e =
-        cudaFuncSetAttribute(xypass_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    init = true;
-  }
+  static unsigned done = 0;
+  cudaError_t e = ensure_smem_attr(xypass_kernel<M>, smem, done);
+  if (e != cudaSuccess) return e;
   dim3 grid((p.nx + XY_TX - 1) / XY_TX, (p.ny + XY_TY - 1) / XY_TY, ze - zb);
   xypass_kernel<M><<<grid, XY_THREADS, smem, s>>>(p, q, qout, w, gz, rout, flag, zb);
 #endif
