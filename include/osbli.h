@@ -6,14 +6,20 @@
  * "OpenSBLI ..." (arXiv 1609.01277), as the paper's generated solver performs
  * it (PAPER.md; "P:n" = line n):
  *   - equations (5)-(9): mass, momentum, energy, stress tensor
- *     tau_ij, heat flux q_j, non-dimensional, constant viscosity (mu = 1);
+ *     tau_ij, heat flux q_j, non-dimensional, constant viscosity (mu = 1) or
+ *     Sutherland's mu(T) (osbli_set_viscosity);
  *   - equation of state and total energy (10)-(11), P:259-266;
  *   - skew-symmetric convective terms (12), with phi = 1, u_i, E;
  *     viscous Laplacians by second-derivative stencils, P:274;
  *     nested derivatives evaluated inner first, P:98;
  *   - central differences of arbitrary even order, P:123;
- *   - forward Euler or the 3-stage low-storage RK3, P:123 and P:164;
- *   - periodic boundaries in every direction, P:141 and P:276;
+ *   - forward Euler or a 3-stage low-storage RK3 (2N or two-register)
+ *     and P:164;
+ *   - periodic boundaries in every direction, or symmetry
+ *     boundaries per direction (osbli_set_boundary);
+ *   - optional steady source term (osbli_set_source, the manufactured-solution
+ *     construction of P:196) and the paper's scalar advection-diffusion
+ *     verification equation (osbli_scalar_*);
  *   - volume-averaged kinetic energy and enstrophy, plus the viscous
  *     dissipation rate (reading D-12).
  * DESIGN.md §3 lists every reading of a point the paper leaves open.
