@@ -83,10 +83,6 @@ __device__ __forceinline__ int zread(const KParams &p, int z, int &flip) {
   flip = 0;
   return max(-p.G, min(z, p.nz - 1 + p.G));
 }
-__device__ __forceinline__ int zread(const KParams &p, int z) {
-  int f;
-  return zread(p, z, f);
-}
 // compile-time variant of bmap: SYM = false is the plain periodic wrap
 template <bool SYM>
 __device__ __forceinline__ int bmap_t(int i, int n, int sym, int &flip) {
