@@ -131,6 +131,10 @@ int osbli_nccl_unique_id(void *id_out);
  *   transfer t receive. */
 int osbli_slab_bounds(int nz, int nranks, int rank, int *z0, int *nz_local);
 int osbli_ghost_plan(int rank, int nranks, int nz_local, int m, int *plan);
+/* The plan with symmetry boundaries in z (symz != 0): the transfers across the
+ * periodic wrap get peer -1 (no send / no receive); the ghost planes they would
+ * have filled are the mirrored own planes, rho u_z negated. */
+int osbli_ghost_plan_sym(int rank, int nranks, int nz_local, int m, int symz, int *plan);
 
 /* Single-GPU test transport: create nslabs handles (out[0..nslabs-1]) that
  * split nz exactly like osbli_create_dist and exchange ghost planes by device
@@ -173,8 +177,9 @@ int osbli_step(osbli_ctx *h, int n);
 int osbli_diagnostics(osbli_ctx *h, osbli_diag *out);
 
 /* Boundary condition of direction dir (0 = x, 1 = y, 2 = z), both ends; takes
- * effect at the next stage.  Symmetry in z is not built for slab-decomposed
- * handles (OSBLI_E_UNSUPPORTED). */
+ * effect at the next stage.  On slab-decomposed handles symmetry in z must be
+ * set on every rank: the outer slabs then mirror their own planes instead of
+ * exchanging across the periodic wrap. */
 int osbli_set_boundary(osbli_ctx *h, int dir, int bc);
 
 /* Viscosity law (OSBLI_VISC_*); suth = S/T_ref > 0 for Sutherland (ignored for

@@ -200,10 +200,16 @@ void slab_partition(int nz, int nranks, int rank, int *z0, int *nzl) {
 //   transfer 1: send local planes [nzl-m, nzl)     to the rank above,
 //               receive into ghost planes [-m, 0)    from the rank below.
 // plan = {send_peer, send_plane, recv_peer, recv_plane} x 2 (local plane indices).
-void ghost_plan(int rank, int nranks, int nzl, int m, int plan[8]) {
+void ghost_plan(int rank, int nranks, int nzl, int m, int plan[8], bool symz = false) {
   const int up = (rank + 1) % nranks, dn = (rank - 1 + nranks) % nranks;
   const int p[8] = {dn, 0, up, nzl, up, nzl - m, dn, -m};
   for (int i = 0; i < 8; ++i) plan[i] = p[i];
+  if (symz) {
+    // symmetry in z: no transfer across the periodic wrap between the
+    // last and the first slab (peer -1); those ghosts mirror the own planes
+    if (rank == 0) plan[0] = plan[6] = -1;           // t=0 send down, t=1 receive from below
+    if (rank == nranks - 1) plan[2] = plan[4] = -1;  // t=0 receive from above, t=1 send up
+  }
 }
 
 // z ghost planes of Q buffer `q` from the neighbouring slabs, over NCCL
@@ -215,31 +221,39 @@ int exchange_ghosts(osbli_ctx *h, double *q, cudaStream_t st = nullptr) {
   const int G = h->m;
   const size_t plane = 5 * (size_t)h->nx * h->ny;
   const size_t cnt = (size_t)G * plane;
+  // symmetry in z: the transfers across the periodic wrap (between the
+  // first and the last slab) are absent from the plan (peer -1); those ghost
+  // planes are mirrors of the outer slabs' own interior planes
+  const bool symz = h->base.sym[2] != 0;
   int plan[8];
-  ghost_plan(h->rank, h->nranks, h->nz, G, plan);
+  ghost_plan(h->rank, h->nranks, h->nz, G, plan, symz);
   auto at = [&](double *base, int local_plane) { return base + (size_t)(local_plane + G) * plane; };
   if (h->comm) {
     NK(h, ncclGroupStart());
     for (int t = 0; t < 2; ++t) {
-      NK(h, ncclSend(at(q, plan[4 * t + 1]), cnt, ncclDouble, plan[4 * t + 0], h->comm, st));
-      NK(h, ncclRecv(at(q, plan[4 * t + 3]), cnt, ncclDouble, plan[4 * t + 2], h->comm, st));
+      if (plan[4 * t + 0] >= 0)
+        NK(h, ncclSend(at(q, plan[4 * t + 1]), cnt, ncclDouble, plan[4 * t + 0], h->comm, st));
+      if (plan[4 * t + 2] >= 0)
+        NK(h, ncclRecv(at(q, plan[4 * t + 3]), cnt, ncclDouble, plan[4 * t + 2], h->comm, st));
     }
     NK(h, ncclGroupEnd());
-    return OSBLI_OK;
-  }
-  if (h->loop) {
+  } else if (h->loop) {
     // I receive what my peer sends under the same transfer index: for
     // transfer t the source is peer plan[4t+2]'s plane given by ITS plan.
     for (int t = 0; t < 2; ++t) {
+      if (plan[4 * t + 2] < 0) continue;
       osbli_ctx *src = h->loop->members[plan[4 * t + 2]];
       int splan[8];
-      ghost_plan(src->rank, src->nranks, src->nz, G, splan);
+      ghost_plan(src->rank, src->nranks, src->nz, G, splan, symz);
       CK(h, cudaMemcpyAsync(at(q, plan[4 * t + 3]), at(src->b.q[src->cur], splan[4 * t + 1]),
                             cnt * sizeof(double), cudaMemcpyDeviceToDevice, st));
     }
-    return OSBLI_OK;
+  } else {
+    return fail(h, OSBLI_E_STATE, "distributed handle without a transport");
   }
-  return fail(h, OSBLI_E_STATE, "distributed handle without a transport");
+  if (plan[6] < 0) CK(h, osbli::launch_mirror_ghosts(h->base, q, 0, st, &h->launches));
+  if (plan[2] < 0) CK(h, osbli::launch_mirror_ghosts(h->base, q, 1, st, &h->launches));
+  return OSBLI_OK;
 }
 
 int check_flag(osbli_ctx *h) {
@@ -528,9 +542,13 @@ int osbli_slab_bounds(int nz, int nranks, int rank, int *z0, int *nz_local) {
 }
 
 int osbli_ghost_plan(int rank, int nranks, int nz_local, int m, int *plan) {
+  return osbli_ghost_plan_sym(rank, nranks, nz_local, m, 0, plan);
+}
+
+int osbli_ghost_plan_sym(int rank, int nranks, int nz_local, int m, int symz, int *plan) {
   if (nranks < 1 || rank < 0 || rank >= nranks || m < 1 || nz_local < m || !plan)
     return OSBLI_E_INVAL;
-  ghost_plan(rank, nranks, nz_local, m, plan);
+  ghost_plan(rank, nranks, nz_local, m, plan, symz != 0);
   return OSBLI_OK;
 }
 
@@ -604,8 +622,6 @@ int osbli_set_boundary(osbli_ctx *h, int dir, int bc) {
   if (u) return u;
   if (dir < 0 || dir > 2 || (bc != OSBLI_BC_PERIODIC && bc != OSBLI_BC_SYMMETRY))
     return fail(h, OSBLI_E_INVAL, "bad direction or boundary type");
-  if (dir == 2 && bc == OSBLI_BC_SYMMETRY && h->nranks > 1)
-    return fail(h, OSBLI_E_UNSUPPORTED, "symmetry in z is not built for slab decompositions");
   h->base.sym[dir] = bc;
   return OSBLI_OK;
 }

@@ -364,6 +364,24 @@ __global__ void __launch_bounds__(256, 4) divh_kernel(const KParams p,
   if (bad) atomicOr(flag, 1u);
 }
 
+// ------------------------------------------------------------------ symmetric z on slabs
+// ghost plane -k <- interior k-1 (side 0), nz-1+k <- nz-k (side 1), k = 1..G;
+// rho u_z (field 3) is odd under the mirror
+__global__ void mirror_ghosts_kernel(const KParams p, double *__restrict__ q, int side) {
+  const size_t FS = (size_t)p.nx * p.ny;
+  const size_t n = (size_t)p.G * 5 * FS;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < n;
+       t += (size_t)gridDim.x * blockDim.x) {
+    const int k = 1 + (int)(t / (5 * FS));
+    const size_t rem = t % (5 * FS);
+    const int f = (int)(rem / FS);
+    const int zg = side == 0 ? -k : p.nz - 1 + k;
+    const int zi = side == 0 ? k - 1 : p.nz - k;
+    const double v = q[qplane(p, zi) + rem];
+    q[qplane(p, zg) + rem] = f == 3 ? -v : v;
+  }
+}
+
 // ------------------------------------------------------------------ layout conversion
 __global__ void abi_to_internal_kernel(const KParams p, const double *__restrict__ src,
                                        double *__restrict__ q) {
@@ -549,6 +567,16 @@ cudaError_t launch_divh(const KParams &p, double *q_out, double *w, double *r_ou
     default: return cudaErrorInvalidValue;
   }
 #undef DCALL
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mirror_ghosts(const KParams &p, double *q, int side, cudaStream_t s,
+                                 long long *launches) {
+  ++*launches;
+  const size_t n = (size_t)p.G * 5 * p.nx * p.ny;
+  size_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  mirror_ghosts_kernel<<<(int)blocks, 256, 0, s>>>(p, q, side);
   return cudaGetLastError();
 }
 

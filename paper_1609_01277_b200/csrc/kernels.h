@@ -62,6 +62,12 @@ cudaError_t launch_divh(const KParams &p, double *q_out, double *w, double *r_ou
                         unsigned int *flag, int z_begin, int z_end, cudaStream_t s,
                         long long *launches);
 
+// Symmetry boundary in z on a slab handle: fill the m ghost planes of the
+// low (side 0) or high (side 1) domain face with the mirrored interior planes,
+// rho u_z negated.  q is a Q buffer [nz + 2G][5][ny][nx].
+cudaError_t launch_mirror_ghosts(const KParams &p, double *q, int side, cudaStream_t s,
+                                 long long *launches);
+
 // z-pass restricted to planes [z_begin, z_end) (for boundary-first overlap).
 cudaError_t launch_zpass(const KParams &p, const double *q_in, double *w, double *gz,
                          int z_begin, int z_end, cudaStream_t s, long long *launches);

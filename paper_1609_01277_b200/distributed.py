@@ -15,26 +15,42 @@ from __future__ import annotations
 import os
 
 
-def exchange_ghosts_torch(q_ghosted, m: int, rank: int, nranks: int):
-    """Execute the library's ghost plan (osbli_ghost_plan) on a
-    [nz_local + 2m, ...] torch tensor (ghost planes at both ends) with
-    torch.distributed point-to-point calls (any backend).  The CPU (gloo)
-    tests use it to check the decomposition logic of the C library."""
+def exchange_ghosts_torch(q_ghosted, m: int, rank: int, nranks: int, symz: bool = False):
+    """Execute the library's ghost plan (osbli_ghost_plan_sym) on a
+    [nz_local + 2m, 5, ...] torch tensor (ghost planes at both ends) with
+    torch.distributed point-to-point calls (any backend); with symmetry in z the
+    outer faces get the mirrored own planes (field 3, rho u_z, negated), as the
+    library's mirror kernel does.  The CPU (gloo) tests use it to check the
+    decomposition logic of the C library."""
     import torch.distributed as dist
 
     from .native import ghost_plan
     nzl = q_ghosted.shape[0] - 2 * m
+    plan = ghost_plan(rank, nranks, nzl, m, symz)
     ops, recvs = [], []
-    for send_peer, send_plane, recv_peer, recv_plane in ghost_plan(rank, nranks, nzl, m):
-        buf = q_ghosted[send_plane + m:send_plane + 2 * m].contiguous()
-        rbuf = q_ghosted[recv_plane + m:recv_plane + 2 * m].clone()
-        ops.append(dist.P2POp(dist.isend, buf, send_peer))
-        ops.append(dist.P2POp(dist.irecv, rbuf, recv_peer))
-        recvs.append((recv_plane, rbuf))
-    for r in dist.batch_isend_irecv(ops):
-        r.wait()
+    for send_peer, send_plane, recv_peer, recv_plane in plan:
+        if send_peer >= 0:
+            buf = q_ghosted[send_plane + m:send_plane + 2 * m].contiguous()
+            ops.append(dist.P2POp(dist.isend, buf, send_peer))
+        if recv_peer >= 0:
+            rbuf = q_ghosted[recv_plane + m:recv_plane + 2 * m].clone()
+            ops.append(dist.P2POp(dist.irecv, rbuf, recv_peer))
+            recvs.append((recv_plane, rbuf))
+    if ops:
+        for r in dist.batch_isend_irecv(ops):
+            r.wait()
     for recv_plane, rbuf in recvs:
         q_ghosted[recv_plane + m:recv_plane + 2 * m] = rbuf
+    sign = None
+    for side, (_, _, recv_peer, _) in ((1, plan[0]), (0, plan[1])):
+        if recv_peer >= 0:
+            continue
+        if sign is None:
+            sign = q_ghosted.new_ones(q_ghosted.shape[1:])
+            sign[3] = -1.0
+        for k in range(1, m + 1):  # ghost -k <- k-1 (low), nzl-1+k <- nzl-k (high)
+            g, i = (m - k, m + k - 1) if side == 0 else (m + nzl - 1 + k, m + nzl - k)
+            q_ghosted[g] = sign * q_ghosted[i]
     return q_ghosted
 
 

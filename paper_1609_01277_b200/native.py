@@ -82,6 +82,7 @@ def load():
     ip = ctypes.POINTER(c_int)
     L.osbli_slab_bounds.argtypes = [c_int, c_int, c_int, ip, ip]
     L.osbli_ghost_plan.argtypes = [c_int, c_int, c_int, c_int, ip]
+    L.osbli_ghost_plan_sym.argtypes = [c_int, c_int, c_int, c_int, c_int, ip]
     L.osbli_create_loopback.argtypes = [c_int, c_int, c_int, c_int, c_double, c_double, c_double,
                                         c_double, c_double, c_double, c_int, c_int,
                                         ctypes.POINTER(H)]
@@ -136,10 +137,11 @@ def slab_bounds(nz: int, nranks: int, rank: int):
     return z0.value, nzl.value
 
 
-def ghost_plan(rank: int, nranks: int, nz_local: int, m: int):
-    """The library's ghost-exchange plan: [(send_peer, send_plane, recv_peer, recv_plane)] x 2."""
+def ghost_plan(rank: int, nranks: int, nz_local: int, m: int, symz: bool = False):
+    """The library's ghost-exchange plan: [(send_peer, send_plane, recv_peer, recv_plane)] x 2;
+    with symmetry in z the transfers across the periodic wrap have peer -1."""
     plan = (ctypes.c_int * 8)()
-    rc = load().osbli_ghost_plan(rank, nranks, nz_local, m, plan)
+    rc = load().osbli_ghost_plan_sym(rank, nranks, nz_local, m, int(symz), plan)
     if rc != 0:
         raise OsbliError(rc, "invalid ghost-plan arguments")
     return [tuple(plan[4 * t:4 * t + 4]) for t in range(2)]

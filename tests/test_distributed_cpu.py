@@ -52,7 +52,7 @@ def test_ghost_plan_is_a_consistent_ring(nranks):
             assert sent_global == ghost_global
 
 
-def _worker(rank, world, port, nz, m, q):
+def _worker(rank, world, port, nz, m, q, symz=False):
     import torch
     import torch.distributed as dist
 
@@ -64,9 +64,20 @@ def _worker(rank, world, port, nz, m, q):
     z0, nzl = slab_bounds(nz, world, rank)
     loc = torch.full((nzl + 2 * m, 5, 6, 7), float("nan"), dtype=torch.float64)
     loc[m:m + nzl] = torch.from_numpy(glob[z0:z0 + nzl])
-    exchange_ghosts_torch(loc, m, rank, world)
-    idx = [(z0 + k) % nz for k in range(-m, nzl + m)]
-    ok = bool(np.array_equal(loc.numpy(), glob[idx]))
+    exchange_ghosts_torch(loc, m, rank, world, symz)
+    if symz:
+        # mirror about the domain faces: rho u_z (field 3) odd
+        exp = []
+        for k in range(-m, nzl + m):
+            g = z0 + k
+            src, s = (-1 - g, -1.0) if g < 0 else ((2 * nz - 1 - g, -1.0) if g >= nz else (g, 1.0))
+            plane = glob[src].copy()
+            plane[3] *= s
+            exp.append(plane)
+        ok = bool(np.array_equal(loc.numpy(), np.stack(exp)))
+    else:
+        idx = [(z0 + k) % nz for k in range(-m, nzl + m)]
+        ok = bool(np.array_equal(loc.numpy(), glob[idx]))
     q.put((rank, ok))
     dist.barrier()
     dist.destroy_process_group()
@@ -79,6 +90,24 @@ def test_gloo_ghost_exchange_matches_periodic_neighbours(world, nz, m):
     q = ctx.Queue()
     port = _free_port()
     procs = [ctx.Process(target=_worker, args=(r, world, port, nz, m, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok in res), res
+
+
+@pytest.mark.parametrize("world,nz,m", [(2, 24, 6), (3, 31, 4), (4, 40, 2)])
+def test_gloo_ghost_exchange_with_symmetry_in_z(world, nz, m):
+    """The symmetric-z plan (osbli_ghost_plan_sym): no transfer across the periodic
+    wrap (sends and receives still pair up), the outer faces mirrored."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, nz, m, q, True))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=120) for _ in range(world)]
