@@ -300,7 +300,7 @@ def main():
     if cfg.get("cons"):
         solver.set_energy_form(osbli.OSBLI_ENERGY_CONSERVATIVE)
     if cfg.get("sym"):
-        for d in range(3 if world == 1 else 2):
+        for d in range(3):
             solver.set_boundary(d, osbli.OSBLI_BC_SYMMETRY)
     stream = torch.cuda.Stream()
     solver.set_stream(stream.cuda_stream)
