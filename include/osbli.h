@@ -188,8 +188,9 @@ int osbli_set_boundary(osbli_ctx *h, int dir, int bc);
 int osbli_set_viscosity(osbli_ctx *h, int law, double suth);
 
 /* Energy-equation form of the viscous work (OSBLI_ENERGY_*).  The conservative
- * form adds one kernel per stage and 4*nz*nx*ny doubles of device scratch; it is
- * not built for slab-decomposed handles (OSBLI_E_UNSUPPORTED). */
+ * form adds one kernel per stage and about 4*nz*nx*ny doubles of device scratch;
+ * on slab-decomposed handles it also exchanges the flux's ghost planes every
+ * stage, and osbli_residual returns OSBLI_E_UNSUPPORTED there. */
 int osbli_set_energy_form(osbli_ctx *h, int form);
 
 /* Steady source term S added to the right-hand side, dQ/dt = R(Q) + S (the

@@ -41,6 +41,7 @@ struct osbli_ctx {
   double *scratch = nullptr;  // velocity for diagnostics, [nz + 2G][3][ny][nx]
   double *nccl_part = nullptr;  // [nranks * max_nz][3] gathered plane partials
   double *src = nullptr;        // optional source S, plane-major [nz][5][ny][nx]
+  double *hflux_alloc = nullptr;  // H_j with ghost planes [nz + 2G][3][ny][nx] (cons form)
   int max_nz = 0;
   int cur = 0;
   long long step_count = 0;
@@ -118,7 +119,8 @@ void free_all(osbli_ctx *h) {
   cudaFree(h->src);
   h->src = nullptr;
   cudaFree(h->base.dtz);
-  cudaFree(h->base.hflux);
+  cudaFree(h->hflux_alloc);
+  h->hflux_alloc = nullptr;
   h->base.dtz = h->base.hflux = nullptr;
   h->b = Bufs{};
   h->scratch = nullptr;
@@ -212,14 +214,18 @@ void ghost_plan(int rank, int nranks, int nzl, int m, int plan[8], bool symz = f
   }
 }
 
-// z ghost planes of Q buffer `q` from the neighbouring slabs, over NCCL
-// (one process per GPU) or by device copies between sibling handles
-// (loopback transport on one GPU).
-int exchange_ghosts(osbli_ctx *h, double *q, cudaStream_t st = nullptr) {
+// z ghost planes of a plane-major buffer with m ghost planes at each end
+// (`base` = its first ghost plane, `nf` fields per plane, field `odd` odd under a
+// z mirror) from the neighbouring slabs, over NCCL (one process per GPU) or by
+// device copies between sibling handles (loopback transport on one GPU);
+// `sibling` picks the same buffer of a sibling handle.
+template <typename Sibling>
+int exchange_planes(osbli_ctx *h, double *base, int nf, int odd, Sibling sibling,
+                    cudaStream_t st) {
   if (h->nranks == 1) return OSBLI_OK;
   if (!st) st = h->stream;
   const int G = h->m;
-  const size_t plane = 5 * (size_t)h->nx * h->ny;
+  const size_t plane = (size_t)nf * h->nx * h->ny;
   const size_t cnt = (size_t)G * plane;
   // symmetry in z: the transfers across the periodic wrap (between the
   // first and the last slab) are absent from the plan (peer -1); those ghost
@@ -227,14 +233,14 @@ int exchange_ghosts(osbli_ctx *h, double *q, cudaStream_t st = nullptr) {
   const bool symz = h->base.sym[2] != 0;
   int plan[8];
   ghost_plan(h->rank, h->nranks, h->nz, G, plan, symz);
-  auto at = [&](double *base, int local_plane) { return base + (size_t)(local_plane + G) * plane; };
+  auto at = [&](double *b, int local_plane) { return b + (size_t)(local_plane + G) * plane; };
   if (h->comm) {
     NK(h, ncclGroupStart());
     for (int t = 0; t < 2; ++t) {
       if (plan[4 * t + 0] >= 0)
-        NK(h, ncclSend(at(q, plan[4 * t + 1]), cnt, ncclDouble, plan[4 * t + 0], h->comm, st));
+        NK(h, ncclSend(at(base, plan[4 * t + 1]), cnt, ncclDouble, plan[4 * t + 0], h->comm, st));
       if (plan[4 * t + 2] >= 0)
-        NK(h, ncclRecv(at(q, plan[4 * t + 3]), cnt, ncclDouble, plan[4 * t + 2], h->comm, st));
+        NK(h, ncclRecv(at(base, plan[4 * t + 3]), cnt, ncclDouble, plan[4 * t + 2], h->comm, st));
     }
     NK(h, ncclGroupEnd());
   } else if (h->loop) {
@@ -245,15 +251,27 @@ int exchange_ghosts(osbli_ctx *h, double *q, cudaStream_t st = nullptr) {
       osbli_ctx *src = h->loop->members[plan[4 * t + 2]];
       int splan[8];
       ghost_plan(src->rank, src->nranks, src->nz, G, splan, symz);
-      CK(h, cudaMemcpyAsync(at(q, plan[4 * t + 3]), at(src->b.q[src->cur], splan[4 * t + 1]),
+      CK(h, cudaMemcpyAsync(at(base, plan[4 * t + 3]), at(sibling(src), splan[4 * t + 1]),
                             cnt * sizeof(double), cudaMemcpyDeviceToDevice, st));
     }
   } else {
     return fail(h, OSBLI_E_STATE, "distributed handle without a transport");
   }
-  if (plan[6] < 0) CK(h, osbli::launch_mirror_ghosts(h->base, q, 0, st, &h->launches));
-  if (plan[2] < 0) CK(h, osbli::launch_mirror_ghosts(h->base, q, 1, st, &h->launches));
+  if (plan[6] < 0) CK(h, osbli::launch_mirror_planes(h->base, base, nf, odd, 0, st, &h->launches));
+  if (plan[2] < 0) CK(h, osbli::launch_mirror_planes(h->base, base, nf, odd, 1, st, &h->launches));
   return OSBLI_OK;
+}
+
+// ghost planes of the current state Q (buffer q = h->b.q[h->cur])
+int exchange_ghosts(osbli_ctx *h, double *q, cudaStream_t st = nullptr) {
+  return exchange_planes(h, q, 5, 3, [](osbli_ctx *s) { return s->b.q[s->cur]; }, st);
+}
+
+// ghost planes of the viscous-work flux H_j (conservative form, D-27): the
+// divergence kernel's z taps read H_z there
+int exchange_hflux(osbli_ctx *h, cudaStream_t st = nullptr) {
+  return exchange_planes(h, h->hflux_alloc, 3, 2, [](osbli_ctx *s) { return s->hflux_alloc; },
+                         st);
 }
 
 int check_flag(osbli_ctx *h) {
@@ -424,7 +442,7 @@ int osbli_get_state_async(osbli_ctx *h, double *q, int on_device) {
 namespace {
 
 // One stage s of the time scheme on handle h: ghost exchange, z-pass, xy-pass.
-int run_stage(osbli_ctx *h, int s, bool exchange = true) {
+int run_stage(osbli_ctx *h, int s, bool exchange = true, bool divh = true) {
   static const double RK_A[3] = {0.0, -5.0 / 9.0, -153.0 / 128.0};
   static const double RK_B[3] = {1.0 / 3.0, 15.0 / 16.0, 8.0 / 15.0};
   static const double RK2R_ALPHA[3] = {2.0 / 3.0, 5.0 / 12.0, 3.0 / 5.0};
@@ -506,11 +524,44 @@ int run_stage(osbli_ctx *h, int s, bool exchange = true) {
                              &h->launches));
   CK(h, osbli::launch_xypass(p, qin, qout, h->b.w, h->b.gz, nullptr, h->b.flag, hi, h->nz,
                              h->stream, &h->launches));
-  if (h->comm) CK(h, cudaEventRecord(h->ev_qready, h->stream));
+  // (with the conservative viscous work Q' is final only after the divergence)
+  if (h->comm && !p.cons) CK(h, cudaEventRecord(h->ev_qready, h->stream));
   CK(h, osbli::launch_xypass(p, qin, qout, h->b.w, h->b.gz, nullptr, h->b.flag, lo, hi, h->stream,
                              &h->launches));
   if (ev) CK(h, cudaEventRecord(ev[2], h->stream));
+  if (p.cons && divh) {
+    // D_z H_z at the slab faces needs the neighbours' H: exchange its ghost planes
+    int r = exchange_hflux(h, h->stream);
+    if (r) return r;
+    CK(h, osbli::launch_divh(p, qout, h->b.w, nullptr, h->b.flag, 0, h->nz, h->stream,
+                             &h->launches));
+    if (h->comm) CK(h, cudaEventRecord(h->ev_qready, h->stream));
+  }
   h->cur ^= 1;
+  return OSBLI_OK;
+}
+
+// the divergence of the viscous-work flux for stage s of a slab handle whose
+// xy-pass ran (run_stage(..., divh = false)) and whose H ghosts are current
+int finish_divh(osbli_ctx *h, int s) {
+  static const double RK_B[3] = {1.0 / 3.0, 15.0 / 16.0, 8.0 / 15.0};
+  static const double RK2R_ALPHA[3] = {2.0 / 3.0, 5.0 / 12.0, 3.0 / 5.0};
+  static const double RK2R_BETA[3] = {1.0 / 4.0, 3.0 / 20.0, 3.0 / 5.0};
+  KParams p = h->base;
+  if (h->scheme == OSBLI_RK3) {
+    p.B = RK_B[s];
+    p.write_w = (s < 2);
+  } else if (h->scheme == OSBLI_RK3_2R) {
+    p.B = RK2R_ALPHA[s];
+    p.beta = RK2R_BETA[s];
+    p.two_reg = 1;
+    p.write_w = (s < 2);
+  } else {
+    p.B = 1.0;
+    p.write_w = 0;
+  }
+  CK(h, osbli::launch_divh(p, h->b.q[h->cur], h->b.w, nullptr, h->b.flag, 0, h->nz, h->stream,
+                           &h->launches));
   return OSBLI_OK;
 }
 
@@ -607,9 +658,20 @@ int osbli_loopback_step(osbli_ctx **hs, int nslabs, int n) {
         int rc = exchange_ghosts(hs[r], hs[r]->b.q[hs[r]->cur]);
         if (rc) return rc;
       }
+      const bool cons = hs[0]->base.cons != 0;
       for (int r = 0; r < nslabs; ++r) {
-        int rc = run_stage(hs[r], s, /*exchange=*/false);
+        int rc = run_stage(hs[r], s, /*exchange=*/false, /*divh=*/!cons);
         if (rc) return rc;
+      }
+      if (cons) {  // every slab's H is written: exchange its ghosts, then the divergence
+        for (int r = 0; r < nslabs; ++r) {
+          int rc = exchange_hflux(hs[r]);
+          if (rc) return rc;
+        }
+        for (int r = 0; r < nslabs; ++r) {
+          int rc = finish_divh(hs[r], s);
+          if (rc) return rc;
+        }
       }
     }
     for (int r = 0; r < nslabs; ++r) ++hs[r]->step_count;
@@ -648,15 +710,17 @@ int osbli_set_energy_form(osbli_ctx *h, int form) {
   if (u) return u;
   if (form != OSBLI_ENERGY_EXPANDED && form != OSBLI_ENERGY_CONSERVATIVE)
     return fail(h, OSBLI_E_INVAL, "bad energy form");
-  if (form == OSBLI_ENERGY_CONSERVATIVE && h->nranks > 1)
-    return fail(h, OSBLI_E_UNSUPPORTED,
-                "the conservative viscous work is not built for slab decompositions");
   const size_t FS = (size_t)h->nx * h->ny;
   if (form == OSBLI_ENERGY_CONSERVATIVE) {
     CK(h, cudaStreamSynchronize(h->stream));
     if (!h->base.dtz) CK(h, cudaMalloc((void **)&h->base.dtz, (size_t)h->nz * FS * sizeof(double)));
-    if (!h->base.hflux)
-      CK(h, cudaMalloc((void **)&h->base.hflux, (size_t)h->nz * 3 * FS * sizeof(double)));
+    if (!h->hflux_alloc) {
+      // H_j with m ghost planes at each end (the slab path exchanges them); the
+      // kernels address it from the first interior plane
+      const size_t G = (size_t)h->base.G;
+      CK(h, cudaMalloc((void **)&h->hflux_alloc, (h->nz + 2 * G) * 3 * FS * sizeof(double)));
+      h->base.hflux = h->hflux_alloc + G * 3 * FS;
+    }
   }
   h->base.cons = form;
   return OSBLI_OK;
@@ -690,6 +754,9 @@ int osbli_residual(osbli_ctx *h, double *R, int on_device) {
   int u = check_usable(h);
   if (u) return u;
   if (!R) return fail(h, OSBLI_E_INVAL, "null output pointer");
+  if (h->base.cons && h->nranks > 1)
+    return fail(h, OSBLI_E_UNSUPPORTED,
+                "the residual hook of a slab handle has no viscous-work flux exchange");
   const size_t n = (size_t)5 * h->nz * h->nx * h->ny;
   double *qin = h->b.q[h->cur];
   int r = exchange_ghosts(h, qin);

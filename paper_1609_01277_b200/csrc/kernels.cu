@@ -367,18 +367,22 @@ __global__ void __launch_bounds__(256, 4) divh_kernel(const KParams p,
 // ------------------------------------------------------------------ symmetric z on slabs
 // ghost plane -k <- interior k-1 (side 0), nz-1+k <- nz-k (side 1), k = 1..G;
 // rho u_z (field 3) is odd under the mirror
-__global__ void mirror_ghosts_kernel(const KParams p, double *__restrict__ q, int side) {
+// (for a buffer of nf fields per plane starting at its first ghost plane; field
+// `odd` is odd under the mirror: rho u_z for Q, H_z for the viscous-work flux)
+__global__ void mirror_ghosts_kernel(const KParams p, double *__restrict__ base, int nf, int odd,
+                                     int side) {
   const size_t FS = (size_t)p.nx * p.ny;
-  const size_t n = (size_t)p.G * 5 * FS;
+  const size_t PL = (size_t)nf * FS;
+  const size_t n = (size_t)p.G * PL;
   for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < n;
        t += (size_t)gridDim.x * blockDim.x) {
-    const int k = 1 + (int)(t / (5 * FS));
-    const size_t rem = t % (5 * FS);
+    const int k = 1 + (int)(t / PL);
+    const size_t rem = t % PL;
     const int f = (int)(rem / FS);
     const int zg = side == 0 ? -k : p.nz - 1 + k;
     const int zi = side == 0 ? k - 1 : p.nz - k;
-    const double v = q[qplane(p, zi) + rem];
-    q[qplane(p, zg) + rem] = f == 3 ? -v : v;
+    const double v = base[(size_t)(zi + p.G) * PL + rem];
+    base[(size_t)(zg + p.G) * PL + rem] = f == odd ? -v : v;
   }
 }
 
@@ -570,14 +574,19 @@ cudaError_t launch_divh(const KParams &p, double *q_out, double *w, double *r_ou
   return cudaGetLastError();
 }
 
-cudaError_t launch_mirror_ghosts(const KParams &p, double *q, int side, cudaStream_t s,
-                                 long long *launches) {
+cudaError_t launch_mirror_planes(const KParams &p, double *base, int nf, int odd, int side,
+                                 cudaStream_t s, long long *launches) {
   ++*launches;
-  const size_t n = (size_t)p.G * 5 * p.nx * p.ny;
+  const size_t n = (size_t)p.G * nf * p.nx * p.ny;
   size_t blocks = (n + 255) / 256;
   if (blocks > 148 * 8) blocks = 148 * 8;
-  mirror_ghosts_kernel<<<(int)blocks, 256, 0, s>>>(p, q, side);
+  mirror_ghosts_kernel<<<(int)blocks, 256, 0, s>>>(p, base, nf, odd, side);
   return cudaGetLastError();
+}
+
+cudaError_t launch_mirror_ghosts(const KParams &p, double *q, int side, cudaStream_t s,
+                                 long long *launches) {
+  return launch_mirror_planes(p, q, 5, 3, side, s, launches);
 }
 
 cudaError_t launch_stage(const KParams &p, const double *q_in, double *q_out, double *w,

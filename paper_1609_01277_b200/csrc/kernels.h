@@ -67,6 +67,10 @@ cudaError_t launch_divh(const KParams &p, double *q_out, double *w, double *r_ou
 // rho u_z negated.  q is a Q buffer [nz + 2G][5][ny][nx].
 cudaError_t launch_mirror_ghosts(const KParams &p, double *q, int side, cudaStream_t s,
                                  long long *launches);
+// The same for a ghosted buffer of nf fields per plane ([nz + 2G][nf][ny][nx],
+// `base` = its first (ghost) plane) whose field `odd` changes sign.
+cudaError_t launch_mirror_planes(const KParams &p, double *base, int nf, int odd, int side,
+                                 cudaStream_t s, long long *launches);
 
 // z-pass restricted to planes [z_begin, z_end) (for boundary-first overlap).
 cudaError_t launch_zpass(const KParams &p, const double *q_in, double *w, double *gz,
