@@ -24,11 +24,33 @@ import sys
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
+
+
+class _StdoutToStderr:
+    """Route the process's C-level stdout (fd 1) to stderr while native code sets
+    up communicators: NCCL prints a version banner there, and rank 0's stdout
+    must carry exactly one JSON line."""
+
+    def __enter__(self):
+        sys.stdout.flush()
+        self._saved = os.dup(1)
+        os.dup2(2, 1)
+        return self
+
+    def __exit__(self, *exc):
+        sys.stdout.flush()
+        os.dup2(self._saved, 1)
+        os.close(self._saved)
+        return False
 sys.path.insert(0, ROOT)
 
 CONFIGS = {
     "tgv256_o12": dict(n=256, order=12, scheme=1, desc="BASELINE configs[3]: TGV 256^3 12th order RK3"),
     "tgv256_o8": dict(n=256, order=8, scheme=1, desc="BASELINE configs[4]: TGV 256^3/GPU 8th order RK3"),
+    "tgv256_o12_slab1": dict(n=256, order=12, scheme=1, slab1=True,
+                             desc="TGV 256^3 12th order RK3 through the distributed path on one "
+                                  "rank (ghost planes over NCCL self send/recv, boundary-first "
+                                  "schedule): the slab path's own cost"),
     "tgv256_o12_strong": dict(n=256, order=12, scheme=1, strong=True,
                               desc="BASELINE configs[3]: TGV 256^3 12th order RK3, strong scaling "
                                    "(one 256^3 box split into z-slabs)"),
@@ -288,13 +310,17 @@ def main():
     from inputs import TGV_PHYS, tgv
     from paper_1609_01277_b200 import perfmodel
 
-    rank, world, local, uid = osbli.init_distributed()
+    with _StdoutToStderr():
+        rank, world, local, uid = osbli.init_distributed()
     torch.cuda.set_device(local)
     # weak scaling (default): 256^3 per GPU, TGV periods tiled in z; strong: one
     # 256^3 box split into z-slabs (BASELINE configs[3])
     nz_glob = n if cfg.get("strong") else n * world
-    solver = osbli.Solver(n, n, nz_glob, cfg["order"], dx, dt, scheme=cfg["scheme"], rank=rank,
-                          nranks=world, unique_id=uid, **TGV_PHYS)
+    if cfg.get("slab1") and world == 1:
+        uid = osbli.nccl_unique_id()
+    with _StdoutToStderr():
+        solver = osbli.Solver(n, n, nz_glob, cfg["order"], dx, dt, scheme=cfg["scheme"],
+                              rank=rank, nranks=world, unique_id=uid, **TGV_PHYS)
     if cfg.get("visc"):
         solver.set_viscosity(osbli.OSBLI_VISC_SUTHERLAND, SUTH)
     if cfg.get("cons"):
@@ -367,8 +393,11 @@ def main():
     qos = [torch.empty_like(qh).pin_memory() for _ in range(NE)]
     e2e_solvers, e2e_streams = [solver], [stream]
     for _ in range(NE - 1):
-        s2 = osbli.Solver(n, n, nz_glob, cfg["order"], dx, dt, scheme=cfg["scheme"], rank=rank,
-                          nranks=world, unique_id=uid, **TGV_PHYS) if world == 1 else None
+        with _StdoutToStderr():
+            s2 = osbli.Solver(n, n, nz_glob, cfg["order"], dx, dt, scheme=cfg["scheme"],
+                              rank=rank, nranks=world,
+                              unique_id=osbli.nccl_unique_id() if cfg.get("slab1") else None,
+                              **TGV_PHYS) if world == 1 else None
         if s2 is None:
             break  # distributed: one communicator per rank; the handles share it in turn
         if cfg.get("visc"):

@@ -34,6 +34,7 @@ static std::vector<cudaStream_t> &g_loop_streams(LoopGroup *g) { return g->strea
 struct osbli_ctx {
   int nx = 0, ny = 0, nz_global = 0, nz = 0, z0 = 0, order = 0, m = 0, scheme = 0;
   int rank = 0, nranks = 1;
+  bool slab = false;  // distributed (ghost-plane) path: nranks > 1, or one rank over NCCL
   double dx = 0, dt = 0, Re = 0, Pr = 0, Minf = 0, gamma = 0;
   int device = 0;
   cudaStream_t stream = nullptr, own_stream = nullptr;
@@ -161,7 +162,7 @@ int create_common(osbli_ctx *h) {
   p.ny = h->ny;
   p.nz = h->nz;
   p.G = G;
-  p.zwrap = (h->nranks == 1) ? 1 : 0;
+  p.zwrap = h->slab ? 0 : 1;
   p.m = h->m;
   double a[osbli::kMaxHalf] = {0}, b[osbli::kMaxHalf + 1] = {0};
   osbli::central_weights(h->m, a, b);
@@ -222,7 +223,7 @@ void ghost_plan(int rank, int nranks, int nzl, int m, int plan[8], bool symz = f
 template <typename Sibling>
 int exchange_planes(osbli_ctx *h, double *base, int nf, int odd, Sibling sibling,
                     cudaStream_t st) {
-  if (h->nranks == 1) return OSBLI_OK;
+  if (!h->slab) return OSBLI_OK;
   if (!st) st = h->stream;
   const int G = h->m;
   const size_t plane = (size_t)nf * h->nx * h->ny;
@@ -336,7 +337,7 @@ int osbli_create_dist(int nx, int ny, int nz, int order, double dx, double dt, d
   int z0 = 0, nzl = 0;
   slab_partition(nz, nranks, rank, &z0, &nzl);
   const int base = nz / nranks, extra = nz % nranks;
-  if (nranks > 1 && base < m) {
+  if ((nranks > 1 || nccl_unique_id) && base < m) {
     g_create_error = "every slab needs at least order/2 planes";
     return OSBLI_E_INVAL;
   }
@@ -344,10 +345,13 @@ int osbli_create_dist(int nx, int ny, int nz, int order, double dx, double dt, d
   if (!h) return OSBLI_E_NOMEM;
   h->nx = nx; h->ny = ny; h->nz_global = nz; h->nz = nzl; h->z0 = z0;
   h->order = order; h->scheme = scheme; h->rank = rank; h->nranks = nranks;
+  // one rank with a unique id runs the distributed path too (its ghost planes come
+  // from itself over NCCL): the NCCL code path on a single GPU
+  h->slab = nranks > 1 || nccl_unique_id != nullptr;
   h->max_nz = base + (extra ? 1 : 0);
   h->dx = dx; h->dt = dt; h->Re = Re; h->Pr = Pr; h->Minf = Minf; h->gamma = gamma;
   int r = create_common(h);
-  if (r == OSBLI_OK && nranks > 1) {
+  if (r == OSBLI_OK && h->slab) {
     ncclUniqueId id;
     std::memcpy(&id, nccl_unique_id, sizeof(id));
     ncclResult_t nr = ncclCommInitRank(&h->comm, nranks, id, rank);
@@ -484,7 +488,7 @@ int run_stage(osbli_ctx *h, int s, bool exchange = true, bool divh = true) {
     ev = &h->events[h->ev_used];
     h->ev_used += 3;
   }
-  if (h->nranks == 1) {
+  if (!h->slab) {
     if (ev) CK(h, cudaEventRecord(ev[0], h->stream));
     CK(h, osbli::launch_zpass(p, qin, wz, h->b.gz, 0, h->nz, h->stream, &h->launches));
     if (ev) CK(h, cudaEventRecord(ev[1], h->stream));
@@ -620,6 +624,7 @@ int osbli_create_loopback(int nx, int ny, int nz, int order, double dx, double d
       slab_partition(nz, nslabs, r, &h->z0, &h->nz);
       h->nx = nx; h->ny = ny; h->nz_global = nz;
       h->order = order; h->scheme = scheme; h->rank = r; h->nranks = nslabs;
+      h->slab = true;
       h->max_nz = nz / nslabs + (nz % nslabs ? 1 : 0);
       h->dx = dx; h->dt = dt; h->Re = Re; h->Pr = Pr; h->Minf = Minf; h->gamma = gamma;
       h->loop = g;
@@ -754,7 +759,7 @@ int osbli_residual(osbli_ctx *h, double *R, int on_device) {
   int u = check_usable(h);
   if (u) return u;
   if (!R) return fail(h, OSBLI_E_INVAL, "null output pointer");
-  if (h->base.cons && h->nranks > 1)
+  if (h->base.cons && h->slab)
     return fail(h, OSBLI_E_UNSUPPORTED,
                 "the residual hook of a slab handle has no viscous-work flux exchange");
   const size_t n = (size_t)5 * h->nz * h->nx * h->ny;
@@ -807,7 +812,7 @@ int osbli_diagnostics(osbli_ctx *h, osbli_diag *out) {
     if (r) return r;
     CK(h, osbli::launch_diagnostics(h->base, qin, h->scratch, h->b.diag_part, h->stream,
                                     &h->launches));
-    if (h->nranks > 1) {
+    if (h->comm) {
       stride = h->max_nz;
       CK(h, cudaMemsetAsync(h->nccl_part, 0, (size_t)3 * h->nranks * h->max_nz * sizeof(double),
                             h->stream));
