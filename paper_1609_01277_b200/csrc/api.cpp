@@ -12,6 +12,7 @@
 #include <nccl.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstdint>
 #include <cstring>
 #include <new>
@@ -35,6 +36,7 @@ struct osbli_ctx {
   int nx = 0, ny = 0, nz_global = 0, nz = 0, z0 = 0, order = 0, m = 0, scheme = 0;
   int rank = 0, nranks = 1;
   bool slab = false;  // distributed (ghost-plane) path: nranks > 1, or one rank over NCCL
+  bool overlap = false;  // boundary-first split schedule (OSBLI_SLAB_OVERLAP=1)
   double dx = 0, dt = 0, Re = 0, Pr = 0, Minf = 0, gamma = 0;
   int device = 0;
   cudaStream_t stream = nullptr, own_stream = nullptr;
@@ -203,6 +205,11 @@ void slab_partition(int nz, int nranks, int rank, int *z0, int *nzl) {
 //   transfer 1: send local planes [nzl-m, nzl)     to the rank above,
 //               receive into ghost planes [-m, 0)    from the rank below.
 // plan = {send_peer, send_plane, recv_peer, recv_plane} x 2 (local plane indices).
+bool slab_overlap_from_env() {
+  const char *v = std::getenv("OSBLI_SLAB_OVERLAP");
+  return v && v[0] == '1';
+}
+
 void ghost_plan(int rank, int nranks, int nzl, int m, int plan[8], bool symz = false) {
   const int up = (rank + 1) % nranks, dn = (rank - 1 + nranks) % nranks;
   const int p[8] = {dn, 0, up, nzl, up, nzl - m, dn, -m};
@@ -348,6 +355,7 @@ int osbli_create_dist(int nx, int ny, int nz, int order, double dx, double dt, d
   // one rank with a unique id runs the distributed path too (its ghost planes come
   // from itself over NCCL): the NCCL code path on a single GPU
   h->slab = nranks > 1 || nccl_unique_id != nullptr;
+  h->overlap = slab_overlap_from_env();
   h->max_nz = base + (extra ? 1 : 0);
   h->dx = dx; h->dt = dt; h->Re = Re; h->Pr = Pr; h->Minf = Minf; h->gamma = gamma;
   int r = create_common(h);
@@ -501,6 +509,33 @@ int run_stage(osbli_ctx *h, int s, bool exchange = true, bool divh = true) {
     h->cur ^= 1;
     return OSBLI_OK;
   }
+  if (!h->overlap) {
+    // Slab decomposition, plain schedule: exchange the ghost planes, then one
+    // z-pass and one xy-pass over the whole slab.  (At 256^2 planes the exchange
+    // is ~30 MB per stage; the split schedule below hides it but costs more in
+    // its six small launches than it saves.)
+    if (h->comm) {
+      int r = exchange_ghosts(h, qin, h->stream);
+      if (r) return r;
+    } else if (exchange) {
+      int r = exchange_ghosts(h, qin);
+      if (r) return r;
+    }
+    if (ev) CK(h, cudaEventRecord(ev[0], h->stream));
+    CK(h, osbli::launch_zpass(p, qin, wz, h->b.gz, 0, h->nz, h->stream, &h->launches));
+    if (ev) CK(h, cudaEventRecord(ev[1], h->stream));
+    CK(h, osbli::launch_xypass(p, qin, qout, h->b.w, h->b.gz, nullptr, h->b.flag, 0, h->nz,
+                               h->stream, &h->launches));
+    if (ev) CK(h, cudaEventRecord(ev[2], h->stream));
+    if (p.cons && divh) {
+      int r = exchange_hflux(h, h->stream);
+      if (r) return r;
+      CK(h, osbli::launch_divh(p, qout, h->b.w, nullptr, h->b.flag, 0, h->nz, h->stream,
+                               &h->launches));
+    }
+    h->cur ^= 1;
+    return OSBLI_OK;
+  }
   // Slab decomposition, boundary first: only the z-pass of the m planes next to
   // each slab face reads ghost planes.  The exchange of Q's boundary planes runs
   // on the comm stream while the interior z-pass runs; the xy-pass writes the
@@ -625,6 +660,7 @@ int osbli_create_loopback(int nx, int ny, int nz, int order, double dx, double d
       h->nx = nx; h->ny = ny; h->nz_global = nz;
       h->order = order; h->scheme = scheme; h->rank = r; h->nranks = nslabs;
       h->slab = true;
+      h->overlap = slab_overlap_from_env();
       h->max_nz = nz / nslabs + (nz % nslabs ? 1 : 0);
       h->dx = dx; h->dt = dt; h->Re = Re; h->Pr = Pr; h->Minf = Minf; h->gamma = gamma;
       h->loop = g;
