@@ -17,8 +17,17 @@
 // (cp.async), so the HBM latency hides behind the FP64 work.  Each thread
 // produces RZ = 4 consecutive z outputs of its column from register windows.
 constexpr int ZP_TX = 32;
-constexpr int ZP_TZ = 32;
-constexpr int ZP_RZ = 4;
+#ifndef OSBLI_ZP_TZ
+#define OSBLI_ZP_TZ 32
+#endif
+#ifndef OSBLI_ZP_RZ
+#define OSBLI_ZP_RZ 4
+#endif
+#ifndef OSBLI_ZP_MINB
+#define OSBLI_ZP_MINB 1
+#endif
+constexpr int ZP_TZ = OSBLI_ZP_TZ;  // planes per chunk
+constexpr int ZP_RZ = OSBLI_ZP_RZ;  // z outputs per thread
 constexpr int ZP_THREADS = 32 * (ZP_TZ / ZP_RZ);  // 256
 constexpr int ZP_NF = 13;
 // staged operand slots
@@ -118,7 +127,7 @@ __device__ __forceinline__ double d2w(const KParams &p, const double (&v)[ZP_RZ 
 // 2: equation variants (mu(T), conservative viscous work; D-26, D-27) with
 // run-time boundary handling.  Separate instantiations keep the default path lean.
 template <int M, int ZF>
-__global__ void __launch_bounds__(ZP_THREADS, 1)
+__global__ void __launch_bounds__(ZP_THREADS, OSBLI_ZP_MINB)
     zpass_kernel(const KParams p, const double *__restrict__ q, double *__restrict__ w,
                  double *__restrict__ gz, int z_begin, int z_end, int seg_len) {
   constexpr bool SYMZ = ZF != 0;
