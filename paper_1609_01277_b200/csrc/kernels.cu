@@ -142,6 +142,12 @@ __device__ __forceinline__ double sutherland_dmu(const KParams &p, double T, dou
   return mu * (1.5 * rcp_rho(T) - rcp_rho(T + p.suth));
 }
 
+// stencil sums: one dependent FMA chain per output (the four outputs of a register
+// window are independent); 2 interleaves two partial sums per output
+#ifndef OSBLI_STENCIL_CHAINS
+#define OSBLI_STENCIL_CHAINS 1
+#endif
+
 // second derivatives in first differences (D-22); 0 selects the (f+ + f-) - 2f form
 #ifndef OSBLI_D2_SBP
 #define OSBLI_D2_SBP 1

@@ -88,14 +88,15 @@ __device__ __forceinline__ void zwindow(const double *S, int f, int slot0, int l
 
 template <int M>
 __device__ __forceinline__ double d1w(const KParams &p, const double (&v)[ZP_RZ + 2 * M], int j) {
-  // two interleaved partial sums halve the dependent FMA chain
+  // one accumulator per output (the four outputs of a window supply the ILP;
+  // OSBLI_STENCIL_CHAINS = 2 interleaves two partial sums)
   double s0 = 0.0, s1 = 0.0;
 #pragma unroll
   for (int k = 1; k <= M; ++k) {
-    if (k & 1) s0 = fma(p.a[k - 1], v[j + M + k] - v[j + M - k], s0);
+    if (OSBLI_STENCIL_CHAINS == 1 || (k & 1)) s0 = fma(p.a[k - 1], v[j + M + k] - v[j + M - k], s0);
     else s1 = fma(p.a[k - 1], v[j + M + k] - v[j + M - k], s1);
   }
-  return s0 + s1;
+  return OSBLI_STENCIL_CHAINS == 1 ? s0 : s0 + s1;
 }
 
 // exactly zero on a constant window (D-22)
@@ -106,20 +107,20 @@ __device__ __forceinline__ double d2w(const KParams &p, const double (&v)[ZP_RZ 
 #pragma unroll
   for (int l = 0; l < M; ++l) {
     const double t = (v[j + M + l + 1] - v[j + M + l]) - (v[j + M - l] - v[j + M - l - 1]);
-    if (l & 1) s1 = fma(p.cb[l], t, s1);
+    if (OSBLI_STENCIL_CHAINS != 1 && (l & 1)) s1 = fma(p.cb[l], t, s1);
     else s0 = fma(p.cb[l], t, s0);
   }
-  return s0 + s1;
+  return OSBLI_STENCIL_CHAINS == 1 ? s0 : s0 + s1;
 #else
   const double c = v[j + M];
   double s0 = 0.0, s1 = 0.0;
 #pragma unroll
   for (int k = 1; k <= M; ++k) {
     const double t = fma(-2.0, c, v[j + M + k] + v[j + M - k]);
-    if (k & 1) s0 = fma(p.b[k], t, s0);
+    if (OSBLI_STENCIL_CHAINS == 1 || (k & 1)) s0 = fma(p.b[k], t, s0);
     else s1 = fma(p.b[k], t, s1);
   }
-  return s0 + s1;
+  return OSBLI_STENCIL_CHAINS == 1 ? s0 : s0 + s1;
 #endif
 }
 
