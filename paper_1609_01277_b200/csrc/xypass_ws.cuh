@@ -209,14 +209,16 @@ __device__ __forceinline__ void conservative_dir(const KParams &p, const double 
                                                  double (&R)[5][4]) {
   using Gm = XYGeom<M>;
   constexpr int W = Gm::W;
-  double ud[W], pw[W], v[W], t[W];
+  // hu = u_d / 2 (exact halving): every skew half and flux below uses it, so the
+  // factors 1/2 cost nothing per term; (1/2 e + p) u_d = (e + 2p) hu exactly
+  double hu[W], pw[W], v[W], t[W];
   double heat[4];
   {
     double r[W];
     ldwin<W>(PR + XP_R * Gm::FSZ + base, st, r);
     ldwin<W>(S + (XF_M0 + DIR) * Gm::FSZ + base, st, t);
 #pragma unroll
-    for (int k = 0; k < W; ++k) ud[k] = __dmul_rn(t[k], r[k]);
+    for (int k = 0; k < W; ++k) hu[k] = 0.5 * __dmul_rn(t[k], r[k]);
 #pragma unroll
     for (int j = 0; j < 4; ++j) R[0][j] = -0.5 * wd1<M, W>(p, t, j);
     ldwin<W>(PR + XP_P * Gm::FSZ + base, st, pw);
@@ -229,23 +231,23 @@ __device__ __forceinline__ void conservative_dir(const KParams &p, const double 
   }
   ldwin<W>(S + XF_RHO * Gm::FSZ + base, st, v);
 #pragma unroll
-  for (int j = 0; j < 4; ++j) R[0][j] = fma(-0.5 * ud[j + M], wd1<M, W>(p, v, j), R[0][j]);
+  for (int j = 0; j < 4; ++j) R[0][j] = fma(-hu[j + M], wd1<M, W>(p, v, j), R[0][j]);
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
     ldwin<W>(S + (XF_M0 + i) * Gm::FSZ + base, st, v);
 #pragma unroll
     for (int k = 0; k < W; ++k)
-      t[k] = (i == DIR) ? fma(0.5 * v[k], ud[k], pw[k]) : __dmul_rn(0.5 * v[k], ud[k]);
+      t[k] = (i == DIR) ? fma(v[k], hu[k], pw[k]) : __dmul_rn(v[k], hu[k]);
 #pragma unroll
     for (int j = 0; j < 4; ++j)
-      R[1 + i][j] = -fma(0.5 * ud[j + M], wd1<M, W>(p, v, j), wd1<M, W>(p, t, j));
+      R[1 + i][j] = -fma(hu[j + M], wd1<M, W>(p, v, j), wd1<M, W>(p, t, j));
   }
   ldwin<W>(S + XF_E * Gm::FSZ + base, st, v);
 #pragma unroll
-  for (int k = 0; k < W; ++k) t[k] = __dmul_rn(fma(0.5, v[k], pw[k]), ud[k]);
+  for (int k = 0; k < W; ++k) t[k] = __dmul_rn(fma(2.0, pw[k], v[k]), hu[k]);
 #pragma unroll
   for (int j = 0; j < 4; ++j)
-    R[4][j] = -fma(0.5 * ud[j + M], wd1<M, W>(p, v, j), wd1<M, W>(p, t, j));
+    R[4][j] = -fma(hu[j + M], wd1<M, W>(p, v, j), wd1<M, W>(p, t, j));
   if (HEAT) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) R[4][j] += heat[j];
