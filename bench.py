@@ -388,7 +388,7 @@ def main():
     # step copies its input state in from the host and its result back out.
     # NE handles on their own streams take the steps in turn, so the host copies
     # of one (PCIe, both directions) overlap the steps of the others.
-    NE = 3
+    NE = int(os.environ.get("OSBLI_E2E_HANDLES", "3"))
     qh = torch.from_numpy(np.ascontiguousarray(Qfull)).pin_memory()
     qos = [torch.empty_like(qh).pin_memory() for _ in range(NE)]
     e2e_solvers, e2e_streams = [solver], [stream]
