@@ -82,9 +82,16 @@ def perturbed_tgv(nx, ny, nz, dx=None, seed=1609012770, amp=1e-3, kmax=4, gamma=
     base_p = 1.0 / (gamma * Minf ** 2) + (np.cos(2 * ax) + np.cos(2 * ay)) * (2.0 + np.cos(2 * az)) / 16.0
     scale = [1.0, 1.0, 1.0, 1.0, 1.0 / (gamma * Minf ** 2)]  # rho, u0, u1, u2, p
     fields = [gamma * Minf ** 2 * base_p, base_u0, base_u1, base_u2, base_p]
+    # the perturbation sum_k ca cos(k.a) + cb sin(k.a) = Re sum_k (ca - i cb) e^{i k.a},
+    # evaluated separably (1D exponentials per direction, then two small
+    # contractions), so that full-size grids (256^3) are generated in seconds
+    ex = np.exp(1j * np.outer(np.arange(0, kmax + 1), 2 * math.pi * np.arange(nx) / nx))
+    ks = np.arange(-kmax, kmax + 1)
+    ey = np.exp(1j * np.outer(ks, 2 * math.pi * np.arange(ny) / ny))
+    ez = np.exp(1j * np.outer(ks, 2 * math.pi * np.arange(nz) / nz))
     ctr = 0
     for f in range(5):
-        pert = np.zeros_like(X)
+        C = np.zeros((len(ks), len(ks), kmax + 1), dtype=complex)  # [kz][ky][kx]
         for kx in range(0, kmax + 1):
             for ky in range(-kmax, kmax + 1):
                 for kz in range(-kmax, kmax + 1):
@@ -93,8 +100,10 @@ def perturbed_tgv(nx, ny, nz, dx=None, seed=1609012770, amp=1e-3, kmax=4, gamma=
                     ca = _uniform(seed, ctr)
                     cb = _uniform(seed, ctr + 1)
                     ctr += 2
-                    ph = kx * ax + ky * ay + kz * az
-                    pert += ca * np.cos(ph) + cb * np.sin(ph)
+                    C[kz + kmax, ky + kmax, kx] = ca - 1j * cb
+        A = C @ ex                                   # [kz][ky][x]
+        B = np.einsum("ay,zax->zyx", ey, A)          # [kz][y][x]
+        pert = np.real(np.tensordot(ez.T, B, axes=(1, 0)))  # [z][y][x]
         pert /= max(np.max(np.abs(pert)), 1e-300)
         fields[f] = fields[f] + amp * scale[f] * pert
     rho, u0, u1, u2, p = fields

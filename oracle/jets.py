@@ -1,7 +1,7 @@
 """Second-order Taylor jets and the exact continuous residual (TEST INFRASTRUCTURE ONLY).
 
 A jet carries (value, gradient, Hessian) of a smooth field at every grid point,
-propagated exactly through +, -, *, /, sin, cos by the product / quotient /
+propagated exactly through +, -, *, /, sqrt, sin, cos by the product / quotient /
 chain rules.  ``exact_residual`` evaluates the right-hand side of the paper's
 compressible Navier-Stokes equations (5)-(9) with the EOS and total
 energy in conservative divergence form for a manufactured state —
@@ -74,6 +74,14 @@ class Jet:
     def __rtruediv__(self, o):
         return self.recip() * o
 
+    def sqrt(self):
+        """s = sqrt(a) from the product rule applied to s * s = a (no power-law
+        calculus): s.g = a.g / (2 s), s.h = (a.h - 2 s.g (x) s.g) / (2 s)."""
+        s = np.sqrt(self.v)
+        g = self.g / (2.0 * s)
+        h = (self.h - 2.0 * np.einsum("i...,j...->ij...", g, g)) / (2.0 * s)
+        return Jet(s, g, h)
+
 
 def _fn(a: Jet, f, df, d2f):
     v = f(a.v)
@@ -128,9 +136,12 @@ def exact_residual(prim_fn, X, Y, Z, Re, Pr, Minf, gamma, suth=None):
     if suth is None:
         mu, dmu = np.ones_like(T.v), [np.zeros_like(T.v)] * 3
     else:
-        mu = T.v ** 1.5 * (1.0 + suth) / (T.v + suth)
-        mup = mu * (1.5 / T.v - 1.0 / (T.v + suth))
-        dmu = [mup * T.g[j] for j in range(3)]
+        # mu(T) evaluated on the temperature jet: its gradient d mu/dx_j comes
+        # from the product, quotient and square-root rules, not from a retyped
+        # closed form of mu'(T)
+        muj = T * T.sqrt() * (1.0 + suth) / (T + suth)
+        mu = muj.v
+        dmu = [muj.g[j] for j in range(3)]
     S = [[G[i][j] + G[j][i] - (2.0 / 3.0 * div if i == j else 0.0) for j in range(3)]
          for i in range(3)]
     tau = [[nu * mu * S[i][j] for j in range(3)] for i in range(3)]

@@ -68,3 +68,32 @@ def sample_residual(p: core.OracleParams, Q: np.ndarray, points):
         Rb = core.residual(bp, np.ascontiguousarray(box))
         out[t] = Rb[:, centre[2], centre[1], centre[0]]
     return out
+
+
+def sample_block(p: core.OracleParams, Q: np.ndarray, lo, size, scheme: int, nsteps: int):
+    """Oracle Q after `nsteps` on the block of points lo[d] <= i_d < lo[d] + size[d]
+    (indices taken modulo the grid, so a block may straddle the periodic wrap)
+    -> [5][size_z][size_y][size_x].
+
+    The same argument as sample_step, for a block: the box is the block widened
+    by h = S*m points on each side, so every block point is at least h from the
+    box faces and its value is bitwise the full-grid oracle's.  Directions where
+    the box would not be smaller than the grid keep the full periodic extent.
+    """
+    m = p.order // 2
+    S = nsteps * (1 if scheme == 0 else 3)
+    h = S * m
+    Q = np.asarray(Q).reshape(p.shape)
+    n = (p.nx, p.ny, p.nz)
+    idx, sel = [], []
+    for d in range(3):
+        if 2 * h + size[d] >= n[d]:
+            idx.append(np.arange(n[d]))
+            sel.append((np.arange(size[d]) + lo[d]) % n[d])
+        else:
+            idx.append((np.arange(-h, h + size[d]) + lo[d]) % n[d])
+            sel.append(np.arange(h, h + size[d]))
+    box = Q[:, idx[2]][:, :, idx[1]][:, :, :, idx[0]]
+    bp = dataclasses.replace(p, nx=len(idx[0]), ny=len(idx[1]), nz=len(idx[2]))
+    Qb = core.step(bp, np.ascontiguousarray(box), scheme, nsteps)
+    return Qb[:, sel[2]][:, :, sel[1]][:, :, :, sel[0]]

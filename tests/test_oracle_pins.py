@@ -288,6 +288,39 @@ def test_two_register_rk3_is_its_butcher_tableau(oracle_lib):
     assert np.abs(got - other).max() > 1e3 * np.abs(got - Q1).max()
 
 
+def test_low_storage_rk3_is_its_butcher_tableau(oracle_lib):
+    """Default scheme (D-1): the 2N form W <- A_s W + dt R(Q), Q <- Q + B_s W
+    with A = (0, -5/9, -153/128), B = (1/3, 15/16, 8/15) is the explicit RK with
+    c = (0, 1/3, 3/4), a21 = 1/3, a31 = -3/16, a32 = 15/16, b = (1/6, 3/10, 8/15)
+    (Williamson 1980).  The tableau satisfies the four third-order conditions
+    exactly, and one oracle step equals the stage-by-stage Butcher evaluation
+    k_i = R(Q0 + dt sum_j a_ij k_j) built from oracle residual calls (catches a
+    wrong A_s or B_s, or W updated after Q, that the order slope alone misses)."""
+    F = Fraction
+    a21, a31, a32 = F(1, 3), F(-3, 16), F(15, 16)
+    b = (F(1, 6), F(3, 10), F(8, 15))
+    c = (F(0), a21, a31 + a32)
+    assert c[2] == F(3, 4)
+    assert sum(b) == 1
+    assert sum(bi * ci for bi, ci in zip(b, c)) == F(1, 2)
+    assert sum(bi * ci * ci for bi, ci in zip(b, c)) == F(1, 3)
+    assert b[2] * a32 * c[1] == F(1, 6)
+    n = (10, 9, 8)
+    dx, dt = 0.4, 0.02
+    Q0 = perturbed_tgv(*n, dx=dx, amp=0.05, kmax=2)
+    p = oracle_lib.OracleParams(*n, 6, dx, dt=dt, **TGV_PHYS)
+    k1 = oracle_lib.residual(p, Q0)
+    k2 = oracle_lib.residual(p, Q0 + dt * float(a21) * k1)
+    k3 = oracle_lib.residual(p, Q0 + dt * (float(a31) * k1 + float(a32) * k2))
+    Q1 = Q0 + dt * (float(b[0]) * k1 + float(b[1]) * k2 + float(b[2]) * k3)
+    got = oracle_lib.step(p, Q0, 1, 1)
+    scale = np.abs(Q0.reshape(5, -1)).max(axis=1)
+    assert np.all(np.abs((got - Q1).reshape(5, -1)).max(axis=1) / scale < 1e-13)
+    # a perturbed tableau (b2 and b3 swapped) is far from the oracle step
+    Qx = Q0 + dt * (float(b[0]) * k1 + float(b[2]) * k2 + float(b[1]) * k3)
+    assert np.abs(got - Qx).max() > 1e3 * np.abs(got - Q1).max()
+
+
 def test_euler_single_step_definition(oracle_lib):
     """Q1 = Q0 + dt R(Q0) (S:293 example 1 + 0.1*2 = 1.2 generalised)."""
     n = (9, 8, 7)
@@ -353,3 +386,20 @@ def test_windowed_sample_is_bitwise_full_grid(oracle_lib):
     r = windowed.sample_residual(p, Q, pts)
     for t, (i, j, k) in enumerate(pts):
         assert np.array_equal(r[t], R[:, k, j, i])
+
+
+def test_windowed_block_is_bitwise_full_grid(oracle_lib):
+    """The block sampler (full-size GPU parity at 256^3) reproduces the full-grid
+    oracle bitwise, for blocks inside the grid and straddling the periodic wrap,
+    with the box narrower than the grid in some directions and not in others."""
+    from oracle import windowed
+    n = (40, 30, 34)
+    Q = perturbed_tgv(*n, amp=0.02)
+    p = oracle_lib.OracleParams(*n, 4, 2 * math.pi / 40, dt=0.01, **TGV_PHYS)
+    full = oracle_lib.step(p, Q, 1, 1)  # h = 3 * 2 = 6: box 12 + size
+    for lo, size in [((3, 5, 7), (4, 3, 5)), ((37, 28, 31), (6, 4, 5)), ((10, 0, 0), (25, 30, 2))]:
+        b = windowed.sample_block(p, Q, lo, size, 1, 1)
+        ix = [(np.arange(size[d]) + lo[d]) % n[d] for d in range(3)]
+        ref = full[:, ix[2]][:, :, ix[1]][:, :, :, ix[0]]
+        assert b.shape == ref.shape
+        assert np.array_equal(b, ref)

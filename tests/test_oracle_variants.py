@@ -152,3 +152,23 @@ def test_variants_with_symmetry_equal_mirror_doubled(oracle_lib, axes):
                                                                   axes, shape))
     assert np.array_equal(oracle_lib.step(ps, Q, 1, 2),
                           first_half(oracle_lib.step(pp, D, 1, 2), axes, shape))
+
+
+def test_jet_sqrt_is_the_square_root_jet():
+    """The Jet square root (used for mu(T) = T^1.5 (1+S)/(T+S) in the exact
+    residual) against closed forms: sqrt(x^2 + y) has gradient (x, 1/2)/s and
+    Hessian entries d2/dx2 = y/s^3, d2/dxdy = -x/(2 s^3), d2/dy2 = -1/(4 s^3)."""
+    import numpy as np
+    from oracle.jets import coordinate_jets
+    X, Y, Z = np.meshgrid(np.linspace(0.3, 2.0, 5), np.linspace(0.5, 1.5, 4), [0.0], indexing="ij")
+    x, y, z = coordinate_jets(X, Y, Z)
+    s = (x * x + y).sqrt()
+    sv = np.sqrt(X * X + Y)
+    assert np.allclose(s.v, sv, rtol=1e-15, atol=0)
+    assert np.allclose(s.g[0], X / sv, rtol=1e-14, atol=0)
+    assert np.allclose(s.g[1], 0.5 / sv, rtol=1e-14, atol=0)
+    assert np.all(s.g[2] == 0.0)
+    assert np.allclose(s.h[0, 0], Y / sv ** 3, rtol=1e-13, atol=0)
+    assert np.allclose(s.h[0, 1], -X / (2 * sv ** 3), rtol=1e-13, atol=0)
+    assert np.allclose(s.h[1, 0], s.h[0, 1], rtol=0, atol=0)
+    assert np.allclose(s.h[1, 1], -1.0 / (4 * sv ** 3), rtol=1e-13, atol=0)
