@@ -18,10 +18,17 @@ endif
 
 all: $(LIB) oracle/liboracle.so
 
-$(CSRC)/kernels.o: $(CSRC)/kernels.cu $(CSRC)/kernels.h $(wildcard $(CSRC)/*.cuh)
+KHDR := $(CSRC)/kernels.h $(CSRC)/dispatch.h $(wildcard $(CSRC)/*.cuh)
+# order-dependent kernels: one object per stencil half width M (built in parallel)
+KM_OBJS := $(foreach m,1 2 3 4 5 6,$(CSRC)/kernels_m$(m).o)
+
+$(CSRC)/kernels_m%.o: $(CSRC)/kernels_order.cu $(KHDR)
+	$(NVCC) $(NVFLAGS) -DOSBLI_M=$* -c $< -o $@ 2> $(CSRC)/ptxas_m$*.log || (cat $(CSRC)/ptxas_m$*.log; false)
+
+$(CSRC)/kernels.o: $(CSRC)/kernels.cu $(KHDR)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(CSRC)/ptxas.log || (cat $(CSRC)/ptxas.log; false)
 
-$(CSRC)/api.o: $(CSRC)/api.cpp $(CSRC)/kernels.h $(CSRC)/weights.h include/osbli.h
+$(CSRC)/api.o: $(CSRC)/api.cpp $(CSRC)/kernels.h $(CSRC)/dispatch.h $(CSRC)/weights.h include/osbli.h
 	$(NVCC) $(ARCH) -O2 -std=c++17 -Xcompiler -fPIC $(NCCL_INC) -x cu -c $< -o $@
 
 $(CSRC)/scalar.o: $(CSRC)/scalar.cu $(CSRC)/scalar.h
@@ -30,7 +37,7 @@ $(CSRC)/scalar.o: $(CSRC)/scalar.cu $(CSRC)/scalar.h
 $(CSRC)/scalar_api.o: $(CSRC)/scalar_api.cpp $(CSRC)/scalar.h $(CSRC)/weights.h include/osbli.h
 	$(NVCC) $(ARCH) -O2 -std=c++17 -Xcompiler -fPIC -x cu -c $< -o $@
 
-$(LIB): $(CSRC)/kernels.o $(CSRC)/api.o $(CSRC)/scalar.o $(CSRC)/scalar_api.o
+$(LIB): $(CSRC)/kernels.o $(KM_OBJS) $(CSRC)/api.o $(CSRC)/scalar.o $(CSRC)/scalar_api.o
 	$(NVCC) $(ARCH) -shared -o $@ $^ $(NCCL_LIB) -lcudart
 
 oracle/liboracle.so: oracle/oracle.cpp

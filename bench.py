@@ -384,6 +384,22 @@ def main():
     value = npts_glob * args.steps / (ms * 1e-3)
     ms_per_step = ms / args.steps
 
+    # ---- diagnostics of the current state through the public call
+    # (synchronous: kernels, per-plane partials to the host, plane-order sum);
+    # device time from events on the solver stream, and the call's wall time
+    solver.diagnostics()
+    d_ev0, d_ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n_diag = 5
+    torch.cuda.synchronize()
+    t_d = time.perf_counter()
+    d_ev0.record(stream)
+    for _ in range(n_diag):
+        solver.diagnostics()
+    d_ev1.record(stream)
+    torch.cuda.synchronize()
+    diag_wall_ms = (time.perf_counter() - t_d) * 1e3 / n_diag
+    diag_ms = d_ev0.elapsed_time(d_ev1) / n_diag
+
     # ---- end to end through the public API with host buffers (pinned): every
     # step copies its input state in from the host and its result back out.
     # NE handles on their own streams take the steps in turn, so the host copies
@@ -508,6 +524,11 @@ def main():
         "roofline": roof,
         "clocks": clocks,
         "gpu_launches": launches,
+        "diagnostics": {"ms_per_call": diag_ms, "wall_ms_per_call": diag_wall_ms,
+                        "share_of_step": diag_ms / ms_per_step,
+                        "how": "osbli_diagnostics (E_k, enstrophy, dissipation) of the 256^3 "
+                               "state, CUDA events on the solver stream around 5 calls; "
+                               "wall_ms includes the host plane-order sum"},
         "e2e": {"value": e2e_value, "unit": "pt-steps/s", "h2d_bytes_per_step": state_bytes,
                 "d2h_bytes_per_step": state_bytes, "steps": args.e2e_steps,
                 "how": f"osbli_set_state_async (pinned host -> device), osbli_step(1), "

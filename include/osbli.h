@@ -100,6 +100,11 @@ typedef struct {
 } osbli_diag;
 
 /* Create a single-GPU solver on the current CUDA device.
+ * The problem statement of the paper's solver: a grid of N points per
+ * direction with spacing dx (x_i = i dx; reading D-9), central
+ * differences of the given even order, the non-dimensional parameters
+ * Re, Pr, Minf, gamma of equations (5)-(11) (TGV values P:290), the
+ * time step dt and the time scheme.
  *   nx,ny,nz >= 1 grid points; order even, 2..12 (else INVAL / UNSUPPORTED);
  *   dx > 0 isotropic spacing; dt > 0 time step;
  *   Re > 0 (Re = +INFINITY means inviscid: nu = kappa = 0); Pr > 0; Minf > 0;
@@ -147,6 +152,15 @@ int osbli_create_loopback(int nx, int ny, int nz, int order, double dx, double d
                           osbli_ctx **out);
 int osbli_loopback_step(osbli_ctx **hs, int nslabs, int n);
 
+/* Stage schedule of a slab handle (halo exchange per stage, P:141,
+ * P:149): 0 = plain (exchange the ghost planes, then the z-pass and xy-pass over
+ * the slab), 1 = boundary first (the exchange runs on a second stream behind the
+ * interior z-pass; the z-pass of the 2m face planes follows it).  Default: 1 when
+ * the slab has neighbours (nranks > 1 or a loopback group), 0 for one rank;
+ * the environment variable OSBLI_SLAB_OVERLAP=0/1 read at create time overrides
+ * the default.  No effect on single-domain handles; INVAL for other values. */
+int osbli_set_slab_schedule(osbli_ctx *h, int boundary_first);
+
 /* Slab owned by this rank: global planes [*z0, *z0 + *nz_local). */
 int osbli_local_box(const osbli_ctx *h, int *z0, int *nz_local);
 
@@ -154,9 +168,13 @@ int osbli_local_box(const osbli_ctx *h, int *z0, int *nz_local);
  * for all subsequent work; NULL selects the library's own stream. */
 int osbli_set_stream(osbli_ctx *h, void *cuda_stream);
 
-/* Copy the conservative state in / out.  q is [5][nz_local][ny][nx] fp64, on the
- * host (on_device = 0) or on the handle's device (on_device = 1).  set_state
- * resets the RK register and the step counter. */
+/* Copy the conservative state in / out: Q = (rho, rho u, rho v, rho w, rho E),
+ * the variables the paper's equations (5)-(7) advance (rho E by the
+ * total-energy relation (11)).  q is [5][nz_local][ny][nx] fp64, on
+ * the host (on_device = 0) or on the handle's device (on_device = 1).
+ * set_state resets the RK register and the step counter.  Errors: INVAL for a
+ * NULL q, CUDA for a failed copy (the handle is then poisoned); get_state stays
+ * valid on a poisoned handle and returns its last state. */
 int osbli_set_state(osbli_ctx *h, const double *q, int on_device);
 int osbli_get_state(osbli_ctx *h, double *q, int on_device);
 
@@ -167,13 +185,20 @@ int osbli_get_state(osbli_ctx *h, double *q, int on_device);
  * (osbli_sync, or any event recorded after it).  Used to overlap the host
  * copies of several handles with each other's steps. */
 int osbli_set_state_async(osbli_ctx *h, const double *q, int on_device);
-int osbli_get_state_async(osbli_ctx *h, double *q, int on_device);
+int osbli_get_state_async(osbli_ctx *h, double *q, int on_device); /* valid when poisoned */
 
-/* Advance n >= 0 full time steps (3 stages for RK3).  Stream-ordered. */
+/* Advance n >= 0 full time steps: forward Euler, or the paper's 3-stage
+ * low-storage RK3 loop, each stage refreshing the periodic (or
+ * symmetry) halos (reading D-10), evaluating the residual of equations
+ * (5)-(12) and updating the state.  Stream-ordered: returns after
+ * enqueueing; a non-finite value is reported by the next synchronising call.
+ * Errors: INVAL for n < 0, STATE on a poisoned handle, CUDA / COMM for launch
+ * or NCCL failures. */
 int osbli_step(osbli_ctx *h, int n);
 
-/* Diagnostics of the current state (collective over ranks when distributed:
- * every rank gets the same, decomposition-independent numbers). */
+/* Diagnostics of the current state (collective over ranks when
+ * distributed: every rank gets the same, decomposition-independent numbers, and
+ * every rank returns OSBLI_E_NONFINITE if any rank's state went non-finite). */
 int osbli_diagnostics(osbli_ctx *h, osbli_diag *out);
 
 /* Boundary condition of direction dir (0 = x, 1 = y, 2 = z), both ends; takes
@@ -199,11 +224,17 @@ int osbli_set_energy_form(osbli_ctx *h, int form);
  * library keeps its own copy. */
 int osbli_set_source(osbli_ctx *h, const double *S, int on_device);
 
-/* Test hook: dQ/dt = R(Q) (+ S if set) of the current state,
- * [5][nz_local][ny][nx], no update. */
+/* Test hook: dQ/dt = R(Q) (+ S if set) of the current state, the semi-discrete
+ * right-hand side of equations (5)-(9) in the skew-symmetric form (12) with the
+ * expanded viscous terms (D-4, D-5), [5][nz_local][ny][nx],
+ * on the host or the device; no update.  Synchronous. */
 int osbli_residual(osbli_ctx *h, double *R, int on_device);
 
-/* Wait for queued work; surfaces asynchronous errors (NONFINITE, CUDA). */
+/* Wait for queued work; surfaces asynchronous errors (NONFINITE, CUDA).  On a
+ * distributed handle the non-finite check is collective (every rank must call
+ * it; all return NONFINITE if any rank's state went non-finite), so that the
+ * ranks refuse their next step together.  A CUDA or NCCL error aborts the
+ * rank's communicator. */
 int osbli_sync(osbli_ctx *h);
 
 /* Instrumentation.  When enabled, osbli_step brackets every z-pass and xy-pass

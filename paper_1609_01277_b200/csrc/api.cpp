@@ -29,6 +29,7 @@ struct LoopGroup {
   std::vector<osbli_ctx *> members;
   std::vector<cudaStream_t> streams;  // every member's own stream, destroyed with the group
   int live = 0;
+  bool broken = false;  // a member was destroyed: the others can no longer exchange
 };
 static std::vector<cudaStream_t> &g_loop_streams(LoopGroup *g) { return g->streams; }
 
@@ -41,8 +42,9 @@ struct osbli_ctx {
   int device = 0;
   cudaStream_t stream = nullptr, own_stream = nullptr;
   Bufs b{};
-  double *scratch = nullptr;  // velocity for diagnostics, [nz + 2G][3][ny][nx]
+  double *scratch = nullptr;  // diagnostics per-(plane, tile) partials
   double *nccl_part = nullptr;  // [nranks * max_nz][3] gathered plane partials
+  unsigned int *flag_all = nullptr;  // max of the ranks' non-finite flags (device)
   double *src = nullptr;        // optional source S, plane-major [nz][5][ny][nx]
   double *hflux_alloc = nullptr;  // H_j with ghost planes [nz + 2G][3][ny][nx] (cons form)
   int max_nz = 0;
@@ -72,6 +74,13 @@ thread_local std::string g_create_error;
 int fail(osbli_ctx *h, int code, const std::string &msg) {
   h->err = msg;
   if (code == OSBLI_E_CUDA || code == OSBLI_E_COMM || code == OSBLI_E_NONFINITE) h->poisoned = true;
+  // a CUDA or NCCL failure on one rank cannot be agreed on collectively: abort the
+  // communicator so that this rank's pending NCCL work is torn down (the peers'
+  // next collective fails or hangs until their launcher ends them)
+  if ((code == OSBLI_E_CUDA || code == OSBLI_E_COMM) && h->comm) {
+    ncclCommAbort(h->comm);
+    h->comm = nullptr;
+  }
   return code;
 }
 
@@ -119,6 +128,8 @@ void free_all(osbli_ctx *h) {
   cudaFree(h->b.diag_part);
   cudaFree(h->scratch);
   cudaFree(h->nccl_part);
+  cudaFree(h->flag_all);
+  h->flag_all = nullptr;
   cudaFree(h->src);
   h->src = nullptr;
   cudaFree(h->base.dtz);
@@ -136,6 +147,9 @@ int create_common(osbli_ctx *h) {
   const int G = h->m;
   const size_t FS = (size_t)h->nx * h->ny;
   const size_t qn = (size_t)(h->nz + 2 * G) * 5 * FS;
+  // per-plane diagnostics partials, padded to the largest slab: the distributed
+  // path all-gathers max_nz planes from every rank (the tail stays zero)
+  const size_t npart = (size_t)3 * (h->max_nz > h->nz ? h->max_nz : h->nz);
   auto alloc = [&](double **p, size_t n) -> cudaError_t {
     return cudaMalloc((void **)p, n * sizeof(double));
   };
@@ -143,8 +157,9 @@ int create_common(osbli_ctx *h) {
   if ((e = alloc(&h->b.q[0], qn)) != cudaSuccess || (e = alloc(&h->b.q[1], qn)) != cudaSuccess ||
       (e = alloc(&h->b.w, (size_t)h->nz * 5 * FS)) != cudaSuccess ||
       (e = alloc(&h->b.gz, (size_t)h->nz * 3 * FS)) != cudaSuccess ||
-      (e = alloc(&h->scratch, (size_t)(h->nz + 2 * G) * 3 * FS)) != cudaSuccess ||
-      (e = alloc(&h->b.diag_part, (size_t)3 * h->nz)) != cudaSuccess ||
+      (e = alloc(&h->scratch, osbli::diagnostics_scratch(KParams{h->nx, h->ny, h->nz}))) !=
+          cudaSuccess ||
+      (e = alloc(&h->b.diag_part, npart)) != cudaSuccess ||
       (e = cudaMalloc((void **)&h->b.flag, sizeof(unsigned int))) != cudaSuccess) {
     free_all(h);
     cudaGetLastError();
@@ -157,6 +172,7 @@ int create_common(osbli_ctx *h) {
   CK(h, cudaMemsetAsync(h->b.q[1], 0, qn * sizeof(double), h->stream));
   CK(h, cudaMemsetAsync(h->b.w, 0, (size_t)h->nz * 5 * FS * sizeof(double), h->stream));
   CK(h, cudaMemsetAsync(h->b.flag, 0, sizeof(unsigned int), h->stream));
+  CK(h, cudaMemsetAsync(h->b.diag_part, 0, npart * sizeof(double), h->stream));
 
   KParams &p = h->base;
   p = KParams{};
@@ -205,9 +221,15 @@ void slab_partition(int nz, int nranks, int rank, int *z0, int *nzl) {
 //   transfer 1: send local planes [nzl-m, nzl)     to the rank above,
 //               receive into ghost planes [-m, 0)    from the rank below.
 // plan = {send_peer, send_plane, recv_peer, recv_plane} x 2 (local plane indices).
-bool slab_overlap_from_env() {
+// Slab schedule: OSBLI_SLAB_OVERLAP=1 / =0 forces the boundary-first / plain
+// schedule; by default the boundary-first one runs whenever the ghost planes come
+// from other slabs (nslabs > 1), the plain one for a single rank exchanging with
+// itself.  osbli_set_slab_schedule overrides either.
+bool slab_overlap_from_env(int nslabs) {
   const char *v = std::getenv("OSBLI_SLAB_OVERLAP");
-  return v && v[0] == '1';
+  if (v && v[0] == '1') return true;
+  if (v && v[0] == '0') return false;
+  return nslabs > 1;
 }
 
 void ghost_plan(int rank, int nranks, int nzl, int m, int plan[8], bool symz = false) {
@@ -252,6 +274,7 @@ int exchange_planes(osbli_ctx *h, double *base, int nf, int odd, Sibling sibling
     }
     NK(h, ncclGroupEnd());
   } else if (h->loop) {
+    if (h->loop->broken) return fail(h, OSBLI_E_STATE, "a sibling slab of this loopback group was destroyed");
     // I receive what my peer sends under the same transfer index: for
     // transfer t the source is peer plan[4t+2]'s plane given by ITS plan.
     for (int t = 0; t < 2; ++t) {
@@ -282,9 +305,33 @@ int exchange_hflux(osbli_ctx *h, cudaStream_t st = nullptr) {
                          st);
 }
 
+// The non-finite flag, agreed on by every rank of a distributed handle (max over
+// ranks by ncclAllReduce: collective), OR-ed over the members of a loopback group,
+// the handle's own otherwise.  Every rank / member that sees it set is poisoned,
+// so that they all refuse the next step together and none waits on a peer.
 int check_flag(osbli_ctx *h) {
   unsigned int flag = 0;
-  CK(h, cudaMemcpyAsync(&flag, h->b.flag, sizeof(flag), cudaMemcpyDeviceToHost, h->stream));
+  if (h->loop) {
+    if (h->loop->broken) return fail(h, OSBLI_E_STATE, "a sibling slab of this loopback group was destroyed");
+    for (osbli_ctx *m : h->loop->members) {
+      unsigned int f = 0;
+      CK(h, cudaMemcpyAsync(&f, m->b.flag, sizeof(f), cudaMemcpyDeviceToHost, m->stream));
+      CK(h, cudaStreamSynchronize(m->stream));
+      flag |= f;
+    }
+    if (flag) {
+      for (osbli_ctx *m : h->loop->members)
+        fail(m, OSBLI_E_NONFINITE, "a time step produced a non-finite value (loopback group)");
+      return OSBLI_E_NONFINITE;
+    }
+    return OSBLI_OK;
+  }
+  const unsigned int *src = h->b.flag;
+  if (h->comm) {
+    NK(h, ncclAllReduce(h->b.flag, h->flag_all, 1, ncclUint32, ncclMax, h->comm, h->stream));
+    src = h->flag_all;
+  }
+  CK(h, cudaMemcpyAsync(&flag, src, sizeof(flag), cudaMemcpyDeviceToHost, h->stream));
   CK(h, cudaStreamSynchronize(h->stream));
   if (flag) return fail(h, OSBLI_E_NONFINITE, "a time step produced a non-finite value");
   return OSBLI_OK;
@@ -355,7 +402,7 @@ int osbli_create_dist(int nx, int ny, int nz, int order, double dx, double dt, d
   // one rank with a unique id runs the distributed path too (its ghost planes come
   // from itself over NCCL): the NCCL code path on a single GPU
   h->slab = nranks > 1 || nccl_unique_id != nullptr;
-  h->overlap = slab_overlap_from_env();
+  h->overlap = slab_overlap_from_env(nranks);
   h->max_nz = base + (extra ? 1 : 0);
   h->dx = dx; h->dt = dt; h->Re = Re; h->Pr = Pr; h->Minf = Minf; h->gamma = gamma;
   int r = create_common(h);
@@ -367,7 +414,8 @@ int osbli_create_dist(int nx, int ny, int nz, int order, double dx, double dt, d
       h->err = std::string("ncclCommInitRank: ") + ncclGetErrorString(nr);
       r = OSBLI_E_COMM;
     } else if (cudaMalloc((void **)&h->nccl_part, (size_t)3 * nranks * h->max_nz * sizeof(double)) !=
-               cudaSuccess) {
+                   cudaSuccess ||
+               cudaMalloc((void **)&h->flag_all, sizeof(unsigned int)) != cudaSuccess) {
       h->err = "device allocation failed";
       r = OSBLI_E_NOMEM;
     } else if (cudaStreamCreateWithFlags(&h->comm_stream, cudaStreamNonBlocking) != cudaSuccess ||
@@ -445,7 +493,7 @@ int osbli_set_state_async(osbli_ctx *h, const double *q, int on_device) {
   return set_state_impl(h, q, on_device, false);
 }
 int osbli_get_state_async(osbli_ctx *h, double *q, int on_device) {
-  if (h && h->poisoned) return OSBLI_E_STATE;
+  // same policy as osbli_get_state: valid on a poisoned handle (the last state)
   return get_state_impl(h, q, on_device, false);
 }
 
@@ -536,14 +584,15 @@ int run_stage(osbli_ctx *h, int s, bool exchange = true, bool divh = true) {
     h->cur ^= 1;
     return OSBLI_OK;
   }
-  // Slab decomposition, boundary first: only the z-pass of the m planes next to
-  // each slab face reads ghost planes.  The exchange of Q's boundary planes runs
-  // on the comm stream while the interior z-pass runs; the xy-pass writes the
-  // boundary planes of Q' first so that the next stage's exchange overlaps the
-  // interior xy-pass.
+  // Slab decomposition, boundary first: only the z-pass of the m
+  // planes next to each slab face reads ghost planes.  The exchange of Q's
+  // boundary planes runs on the comm stream while the interior z-pass runs; the
+  // z-pass of the 2m face planes (one launch, two ranges) waits for it; the
+  // xy-pass (no z taps) runs over the whole slab.  3 launches per stage instead
+  // of 2; the exchange hides behind nz - 2m planes of z-pass.
   const int m = h->m;
-  const int lo = m < h->nz ? m : h->nz;            // [0, lo): low boundary planes
-  const int hi = h->nz - m > lo ? h->nz - m : lo;  // [hi, nz): high boundary planes
+  const int lo = m < h->nz ? m : h->nz;            // [0, lo): low face planes
+  const int hi = h->nz - m > lo ? h->nz - m : lo;  // [hi, nz): high face planes
   if (h->comm) {
     CK(h, cudaStreamWaitEvent(h->comm_stream, h->ev_qready, 0));
     int r = exchange_ghosts(h, qin, h->comm_stream);
@@ -556,17 +605,10 @@ int run_stage(osbli_ctx *h, int s, bool exchange = true, bool divh = true) {
   if (ev) CK(h, cudaEventRecord(ev[0], h->stream));
   CK(h, osbli::launch_zpass(p, qin, wz, h->b.gz, lo, hi, h->stream, &h->launches));
   if (h->comm) CK(h, cudaStreamWaitEvent(h->stream, h->ev_ghost, 0));
-  CK(h, osbli::launch_zpass(p, qin, wz, h->b.gz, 0, lo, h->stream, &h->launches));
-  CK(h, osbli::launch_zpass(p, qin, wz, h->b.gz, hi, h->nz, h->stream, &h->launches));
+  CK(h, osbli::launch_zpass(p, qin, wz, h->b.gz, 0, lo, h->stream, &h->launches, hi, h->nz));
   if (ev) CK(h, cudaEventRecord(ev[1], h->stream));
-  CK(h, osbli::launch_xypass(p, qin, qout, h->b.w, h->b.gz, nullptr, h->b.flag, 0, lo, h->stream,
-                             &h->launches));
-  CK(h, osbli::launch_xypass(p, qin, qout, h->b.w, h->b.gz, nullptr, h->b.flag, hi, h->nz,
+  CK(h, osbli::launch_xypass(p, qin, qout, h->b.w, h->b.gz, nullptr, h->b.flag, 0, h->nz,
                              h->stream, &h->launches));
-  // (with the conservative viscous work Q' is final only after the divergence)
-  if (h->comm && !p.cons) CK(h, cudaEventRecord(h->ev_qready, h->stream));
-  CK(h, osbli::launch_xypass(p, qin, qout, h->b.w, h->b.gz, nullptr, h->b.flag, lo, hi, h->stream,
-                             &h->launches));
   if (ev) CK(h, cudaEventRecord(ev[2], h->stream));
   if (p.cons && divh) {
     // D_z H_z at the slab faces needs the neighbours' H: exchange its ghost planes
@@ -574,8 +616,9 @@ int run_stage(osbli_ctx *h, int s, bool exchange = true, bool divh = true) {
     if (r) return r;
     CK(h, osbli::launch_divh(p, qout, h->b.w, nullptr, h->b.flag, 0, h->nz, h->stream,
                              &h->launches));
-    if (h->comm) CK(h, cudaEventRecord(h->ev_qready, h->stream));
   }
+  // Q' complete: the next stage's exchange may read its face planes
+  if (h->comm) CK(h, cudaEventRecord(h->ev_qready, h->stream));
   h->cur ^= 1;
   return OSBLI_OK;
 }
@@ -660,7 +703,7 @@ int osbli_create_loopback(int nx, int ny, int nz, int order, double dx, double d
       h->nx = nx; h->ny = ny; h->nz_global = nz;
       h->order = order; h->scheme = scheme; h->rank = r; h->nranks = nslabs;
       h->slab = true;
-      h->overlap = slab_overlap_from_env();
+      h->overlap = slab_overlap_from_env(nslabs);
       h->max_nz = nz / nslabs + (nz % nslabs ? 1 : 0);
       h->dx = dx; h->dt = dt; h->Re = Re; h->Pr = Pr; h->Minf = Minf; h->gamma = gamma;
       h->loop = g;
@@ -716,6 +759,17 @@ int osbli_loopback_step(osbli_ctx **hs, int nslabs, int n) {
       }
     }
     for (int r = 0; r < nslabs; ++r) ++hs[r]->step_count;
+  }
+  return OSBLI_OK;
+}
+
+int osbli_set_slab_schedule(osbli_ctx *h, int boundary_first) {
+  int u = check_usable(h);
+  if (u) return u;
+  if (boundary_first != 0 && boundary_first != 1) return fail(h, OSBLI_E_INVAL, "schedule must be 0 or 1");
+  if (h->slab) {
+    CK(h, cudaStreamSynchronize(h->stream));
+    h->overlap = boundary_first != 0;
   }
   return OSBLI_OK;
 }
@@ -824,8 +878,9 @@ int osbli_diagnostics(osbli_ctx *h, osbli_diag *out) {
   int u = check_usable(h);
   if (u) return u;
   if (!out) return fail(h, OSBLI_E_INVAL, "null output pointer");
-  int r = check_flag(h);
-  if (r) return r;
+  if (h->loop && h->loop->broken)
+    return fail(h, OSBLI_E_STATE, "a sibling slab of this loopback group was destroyed");
+  int r = OSBLI_OK;
   std::vector<double> all;
   std::vector<int> counts;
   int stride = h->nz;
@@ -871,6 +926,10 @@ int osbli_diagnostics(osbli_ctx *h, osbli_diag *out) {
     }
   }
   CK(h, cudaStreamSynchronize(h->stream));
+  // the non-finite flag after every rank has taken part in the collectives above
+  // (collective itself: every rank gets the same answer)
+  r = check_flag(h);
+  if (r) return r;
   // Neumaier sums over planes in global z order
   double s[3] = {0, 0, 0}, c[3] = {0, 0, 0};
   for (int rr = 0; rr < (int)counts.size(); ++rr)
@@ -947,6 +1006,7 @@ void osbli_destroy(osbli_ctx *h) {
     // the group stream belongs to member 0: destroy streams with the last member
     for (auto &m : g->members)
       if (m == h) m = nullptr;
+    g->broken = true;
     if (--g->live == 0) {
       for (cudaStream_t st : g_loop_streams(g)) cudaStreamDestroy(st);
       delete g;

@@ -1,0 +1,135 @@
+// Device helpers shared by the kernel translation units (periodic / mirror
+// index maps, cp.async, fast reciprocals, Sutherland).  Internal linkage: every
+// translation unit gets its own copy.
+#pragma once
+#include <cstdint>
+
+#include "kernels.h"
+
+namespace osbli {
+namespace {
+
+
+
+__device__ __forceinline__ int wrapi(int i, int n) {
+  // periodic index: one conditional shift covers every tile halo when n exceeds
+  // the stencil reach; the modulo only runs for grids smaller than that
+  if (i < 0) i += n;
+  else if (i >= n) i -= n;
+  if ((unsigned)i >= (unsigned)n) {
+    i %= n;
+    if (i < 0) i += n;
+  }
+  return i;
+}
+
+// boundary map of index i in a direction of n points: periodic wrap, or the
+// mirror about the boundary faces (symmetry: ghost -k <-> interior k-1,
+// ghost n-1+k <-> interior n-k); flip = 1 after an odd number of mirrors, where
+// a field's normal vector component changes sign
+__device__ __forceinline__ int bmap(int i, int n, int sym, int &flip) {
+  if (!sym) {
+    flip = 0;
+    return wrapi(i, n);
+  }
+  // one reflection at most (every halo of a grid at least m points wide)
+  if ((unsigned)i < (unsigned)n) {
+    flip = 0;
+    return i;
+  }
+  if (i < 0 && i >= -n) {
+    flip = 1;
+    return -1 - i;
+  }
+  if (i >= n && i < 2 * n) {
+    flip = 1;
+    return 2 * n - 1 - i;
+  }
+  int c = i % (2 * n);
+  if (c < 0) c += 2 * n;
+  flip = c >= n;
+  return flip ? 2 * n - 1 - c : c;
+}
+
+__device__ __forceinline__ size_t qplane(const KParams &p, int z) {
+  return (size_t)(z + p.G) * 5 * (size_t)p.nx * p.ny;
+}
+
+// z index of the plane read for logical plane z (wrap or mirror on one GPU,
+// ghost planes otherwise); flip = 1 when rho u_z changes sign (mirror)
+__device__ __forceinline__ int zread(const KParams &p, int z, int &flip) {
+  if (p.zwrap) return bmap(z, p.nz, p.sym[2], flip);
+  flip = 0;
+  return max(-p.G, min(z, p.nz - 1 + p.G));
+}
+// compile-time variant of bmap: SYM = false is the plain periodic wrap
+template <bool SYM>
+__device__ __forceinline__ int bmap_t(int i, int n, int sym, int &flip) {
+  if (SYM) return bmap(i, n, sym, flip);
+  flip = 0;
+  return wrapi(i, n);
+}
+// compile-time variant: SYM = false is the periodic / ghost-plane read (flip = 0)
+template <bool SYM>
+__device__ __forceinline__ int zread_t(const KParams &p, int z, int &flip) {
+  if (SYM) return zread(p, z, flip);
+  flip = 0;
+  if (p.zwrap) return wrapi(z, p.nz);
+  return max(-p.G, min(z, p.nz - 1 + p.G));
+}
+
+// 8-byte asynchronous global -> shared copy (LDGSTS); completed with cp.async.wait_group
+__device__ __forceinline__ void cp_async8(double *smem, const double *gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+
+// 1/rho without the IEEE division's special-case path: the hardware seed
+// (rcp.approx.ftz.f64) and two Newton steps, accurate to about 1 ulp for the
+// normal, positive densities of the method (not correctly rounded: round-off only)
+#ifndef OSBLI_FAST_RCP
+#define OSBLI_FAST_RCP 1
+#endif
+__device__ __forceinline__ double rcp_rho(double x) {
+#if OSBLI_FAST_RCP
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+#else
+  return 1.0 / x;
+#endif
+}
+
+// Sutherland's law in dimensionless form (D-26): mu(T) = T^1.5 (1 + S)/(T + S),
+// mu(1) = 1, and its derivative mu'(T) = mu (3/(2T) - 1/(T + S))
+// (T^1.5 = T^2 / sqrt(T) from the hardware reciprocal-square-root seed and two
+// Newton steps; reciprocals as rcp_rho: about 1 ulp, round-off only, D-28)
+__device__ __forceinline__ double rsqrt_fast(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double hx = 0.5 * x;
+  y = y * fma(-hx * y, y, 1.5);
+  return y * fma(-hx * y, y, 1.5);
+}
+__device__ __forceinline__ double sutherland_mu(const KParams &p, double T) {
+  return (T * T) * rsqrt_fast(T) * ((1.0 + p.suth) * rcp_rho(T + p.suth));
+}
+__device__ __forceinline__ double sutherland_dmu(const KParams &p, double T, double mu) {
+  return mu * (1.5 * rcp_rho(T) - rcp_rho(T + p.suth));
+}
+
+// stencil sums: one dependent FMA chain per output (the four outputs of a register
+// window are independent); 2 interleaves two partial sums per output
+#ifndef OSBLI_STENCIL_CHAINS
+#define OSBLI_STENCIL_CHAINS 1
+#endif
+
+// second derivatives in first differences (D-22); 0 selects the (f+ + f-) - 2f form
+#ifndef OSBLI_D2_SBP
+#define OSBLI_D2_SBP 1
+#endif
+}  // namespace
+}  // namespace osbli

@@ -72,16 +72,19 @@ cudaError_t launch_mirror_ghosts(const KParams &p, double *q, int side, cudaStre
 cudaError_t launch_mirror_planes(const KParams &p, double *base, int nf, int odd, int side,
                                  cudaStream_t s, long long *launches);
 
-// z-pass restricted to planes [z_begin, z_end) (for boundary-first overlap).
+// z-pass restricted to planes [z_begin, z_end) and, in the same launch, [z_begin1,
+// z_end1) (the two slab faces of the boundary-first schedule).
 cudaError_t launch_zpass(const KParams &p, const double *q_in, double *w, double *gz,
-                         int z_begin, int z_end, cudaStream_t s, long long *launches);
+                         int z_begin, int z_end, cudaStream_t s, long long *launches,
+                         int z_begin1 = 0, int z_end1 = 0);
 // xy-pass restricted to planes [z_begin, z_end).
 cudaError_t launch_xypass(const KParams &p, const double *q_in, double *q_out, double *w,
                           const double *gz, double *r_out, unsigned int *flag, int z_begin,
                           int z_end, cudaStream_t s, long long *launches);
 
 // Per-plane diagnostics partial sums [nz][3] (E_k, enstrophy, dissipation sums).
-// scratch: >= 3*nx*ny*nz doubles (velocity).
+// scratch: >= diagnostics_scratch(p) doubles (per-(plane, tile) partials).
+size_t diagnostics_scratch(const KParams &p);
 cudaError_t launch_diagnostics(const KParams &p, const double *q_in, double *scratch,
                                double *part, cudaStream_t s, long long *launches);
 

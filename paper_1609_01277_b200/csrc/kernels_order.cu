@@ -1,0 +1,416 @@
+// =============================================================================
+// sm_100a fp64 kernels of the OpenSBLI hot path (B200-native).
+//
+// One RK stage = two kernels:
+//   zpass  : every term of the residual that differentiates along z
+//            (D_z, D_zz; P:271-274 skew terms, P:274 Laplacians), written as a
+//            partial residual Rz[5] plus the velocity gradients g_i2 = D_z u_i.
+//            A CTA stages 32 x-columns x (TZ+2m) z-planes of the 13 z-stencil
+//            operands in shared memory (computed once per staged point) and
+//            each thread produces RZ = 4 consecutive z outputs from a register
+//            window (reuse (RZ+2m)/RZ instead of 2m loads per output).
+//   xypass : all x/y terms on a 32x16 plane tile with an m-wide halo in
+//            shared memory (warp-specialised: a cp.async producer warpgroup and
+//            two decoupled consumer groups, xypass_ws.cuh), the mixed
+//            derivatives (commuted so that no z stencil is needed:
+//            D_x D_z u_z = D_x g_22, D_z D_x u_x = D_x g_02, ...; D-7),
+//            the viscous dissipation and heat flux, then the fused low-storage
+//            RK stage update W <- W' + dt R_xy, Q' <- Q + B W and
+//            a non-finite check.
+//   variants: symmetry boundaries (mirror maps, N3), the
+//            two-register RK3 (N2a), Sutherland mu(T) and the conservative
+//            viscous work (+ divh_kernel; N2b, N4), each a separate
+//            instantiation so that the default path stays as it is.
+// All arithmetic is IEEE fp64; tensor cores are not used (a stencil is not a
+// dense contraction).  Periodic wrap in x and y is done in-kernel; in
+// z either in-kernel (one GPU) or through ghost planes (slab decomposition).
+// =============================================================================
+// This translation unit instantiates every order-dependent kernel for one
+// stencil half width M = OSBLI_M (the Makefile compiles it once per M, in
+// parallel); kernels.cu dispatches on the run-time order.
+#include "device_common.cuh"
+#include "dispatch.h"
+
+#ifndef OSBLI_M
+#error "compile with -DOSBLI_M=<stencil half width 1..6>"
+#endif
+
+namespace osbli {
+namespace {
+#include "zpass.cuh"
+#include "xypass_ws.cuh"
+
+// ------------------------------------------------------------------ diagnostics
+// Per-(plane, tile) partial sums of the integrands of the diagnostics (
+// D-11, D-12): 1/2 rho u_j u_j, 1/2 rho |omega|^2 and tau_ij du_i/dx_j, with the
+// velocity gradients g_ij = D_j u_i by the solver's first-derivative stencils.
+// A CTA covers a 32 x 8 tile of the plane and DG_Z consecutive planes: per plane
+// u_i on the tile rows with the x-halo (UX) and on the tile columns with the
+// y-halo (UY) are formed from rho, rho u_i in shared memory (u = m * (1/rho) as in
+// the stepping kernels, D-28); the z taps come from a per-thread register window
+// of u_i along z.  The 256 point values of each plane are reduced in a fixed
+// order (warp butterflies, then the 8 warps in order), so the partial of a
+// (plane, tile) depends on nothing but its data: diag_tiles_kernel then sums the
+// tiles of each plane in tile order, and the host sums the planes in global z
+// order, which makes the numbers independent of the slab decomposition.
+template <int M>
+struct DGGeom {
+  static constexpr int XW = 32 + 2 * M;                       // UX row width
+  static constexpr int NX = DG_TY * XW, NY = (DG_TY + 2 * M) * 32;
+};
+
+// u_i at a staged (x, y) of plane z, with the mirror sign of u_d when the index
+// went through an odd number of mirrors in direction d
+__device__ __forceinline__ void diag_u(const KParams &p, const double *__restrict__ q, int z,
+                                       size_t off, double (&u)[3]) {
+  const size_t FS = (size_t)p.nx * p.ny;
+  const double *qp = q + qplane(p, z) + off;
+  const double r = rcp_rho(__ldg(qp));
+#pragma unroll
+  for (int i = 0; i < 3; ++i) u[i] = __ldg(qp + (1 + i) * FS) * r;
+}
+
+template <int M>
+__global__ void __launch_bounds__(256, 2) diag_kernel(const KParams p, const double *__restrict__ q,
+                                                      double *__restrict__ tpart, int ntiles) {
+  using G = DGGeom<M>;
+  __shared__ double UX[3][G::NX];
+  __shared__ double UY[3][G::NY];
+  __shared__ double red[3][8];
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
+  const int x0 = blockIdx.x * 32, y0 = blockIdx.y * DG_TY;
+  const int tile = blockIdx.y * gridDim.x + blockIdx.x;
+  const int x = x0 + tx, y = y0 + ty;
+  const bool valid = x < p.nx && y < p.ny;
+  const int z0 = blockIdx.z * DG_Z;
+  const int nzo = min(DG_Z, p.nz - z0);
+  const size_t off = (size_t)min(y, p.ny - 1) * p.nx + min(x, p.nx - 1);
+  const size_t FS = (size_t)p.nx * p.ny;
+  // register window of u_i along z at this thread's (x, y)
+  double uz[3][DG_Z + 2 * M];
+#pragma unroll
+  for (int t = 0; t < DG_Z + 2 * M; ++t) {
+    double u[3] = {0.0, 0.0, 0.0};
+    if (t < nzo + 2 * M) {
+      int f;
+      const int zz = zread(p, z0 - M + t, f);
+      diag_u(p, q, zz, off, u);
+      if (f) u[2] = -u[2];
+    }
+#pragma unroll
+    for (int i = 0; i < 3; ++i) uz[i][t] = u[i];
+  }
+#pragma unroll
+  for (int j = 0; j < DG_Z; ++j) {
+    if (j >= nzo) break;
+    const int z = z0 + j;
+    __syncthreads();  // the previous plane's staged values are consumed
+    for (int idx = tid; idx < G::NX + G::NY; idx += 256) {
+      double u[3];
+      int fx = 0, fy = 0;
+      int gx, gy;
+      if (idx < G::NX) {  // UX: row r of the tile, column c of the x-extended row
+        const int r = idx / G::XW, c = idx - r * G::XW;
+        gx = bmap(x0 - M + c, p.nx, p.sym[0], fx);
+        gy = min(y0 + r, p.ny - 1);
+      } else {            // UY: row c of the y-extended tile, column tx
+        const int k = idx - G::NX, c = k >> 5;
+        gx = min(x0 + (k & 31), p.nx - 1);
+        gy = bmap(y0 - M + c, p.ny, p.sym[1], fy);
+      }
+      diag_u(p, q, z, (size_t)gy * p.nx + gx, u);
+      if (fx) u[0] = -u[0];
+      if (fy) u[1] = -u[1];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        if (idx < G::NX) UX[i][idx] = u[i];
+        else UY[i][idx - G::NX] = u[i];
+      }
+    }
+    __syncthreads();
+    double g[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const double *rx = &UX[i][ty * G::XW + tx + M];
+      const double *cy = &UY[i][(ty + M) * 32 + tx];
+      double sx = 0.0, sy = 0.0, sz = 0.0;
+#pragma unroll
+      for (int k = 1; k <= M; ++k) {
+        sx = fma(p.a[k - 1], rx[k] - rx[-k], sx);
+        sy = fma(p.a[k - 1], cy[32 * k] - cy[-32 * k], sy);
+        sz = fma(p.a[k - 1], uz[i][j + M + k] - uz[i][j + M - k], sz);
+      }
+      g[i][0] = sx;
+      g[i][1] = sy;
+      g[i][2] = sz;
+    }
+    double v[3] = {0.0, 0.0, 0.0};
+    if (valid) {
+      const double *qp = q + qplane(p, z) + off;
+      const double rho = __ldg(qp);
+      const double u0 = uz[0][j + M], u1 = uz[1][j + M], u2 = uz[2][j + M];
+      const double ke = u0 * u0 + u1 * u1 + u2 * u2;
+      v[0] = 0.5 * rho * ke;
+      const double w0 = g[2][1] - g[1][2], w1 = g[0][2] - g[2][0], w2 = g[1][0] - g[0][1];
+      v[1] = 0.5 * rho * (w0 * w0 + w1 * w1 + w2 * w2);
+      const double th = g[0][0] + g[1][1] + g[2][2];
+      const double s01 = g[0][1] + g[1][0], s02 = g[0][2] + g[2][0], s12 = g[1][2] + g[2][1];
+      double phi = p.nu * (2.0 * (g[0][0] * g[0][0] + g[1][1] * g[1][1] + g[2][2] * g[2][2]) +
+                           s01 * s01 + s02 * s02 + s12 * s12 - (2.0 / 3.0) * th * th);
+      if (p.visc) {  // tau carries mu(T) (D-26)
+        const double pr = p.gm1 * (__ldg(qp + 4 * FS) - 0.5 * rho * ke);
+        phi *= sutherland_mu(p, p.gM2 * pr * rcp_rho(rho));
+      }
+      v[2] = phi;
+    }
+    // fixed-order reduction of the plane's 256 values
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+    }
+    if (tx == 0) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) red[k][ty] = v[k];
+    }
+    __syncthreads();
+    if (tid < 3) {
+      double t = 0.0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) t += red[tid][w];
+      tpart[((size_t)z * ntiles + tile) * 3 + tid] = t;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ conservative viscous work
+// D_j H_j (H_j = u_i tau_ij from the xy-pass; H_j odd under the mirror of
+// direction j) added to the energy of the finished stage (D-27):
+//   residual: R_E += D;  2N: W_E += dt D (write_w), Q'_E += B dt D;
+//   two-register: Q'_E += alpha dt D, Q_old_E += beta dt D (write_w).
+// A CTA covers a 32 x 8 tile of the plane and marches through DH_Z planes:
+// per plane H_x (tile rows + x halo) and H_y (tile columns + y halo) are staged in
+// shared memory (the next plane's values are loaded into registers while the
+// current one is computed); H_z comes from a per-thread register window along z.
+constexpr int DH_Z = 8;
+template <int M>
+struct DHGeom {
+  static constexpr int XW = 32 + 2 * M;                       // H_x row width
+  static constexpr int NX = 8 * XW, NY = (8 + 2 * M) * 32;    // staged elements
+  static constexpr int PER = (NX + NY + 255) / 256;           // per thread
+};
+template <int M, bool SYM>
+__device__ __forceinline__ void divh_fetch(const KParams &p, const double *__restrict__ H, int z,
+                                           int x0, int y0, int tid, double (&v)[DHGeom<M>::PER]) {
+  using G = DHGeom<M>;
+  const size_t FS = (size_t)p.nx * p.ny;
+  const double *hp = H + (size_t)z * 3 * FS;
+#pragma unroll
+  for (int r = 0; r < G::PER; ++r) {
+    const int idx = tid + 256 * r;
+    v[r] = 0.0;
+    if (idx < G::NX) {  // H_x: row ty, column c of the x-extended row
+      const int ty = idx / G::XW, c = idx - ty * G::XW;
+      int f;
+      const int gx = bmap_t<SYM>(x0 - M + c, p.nx, p.sym[0], f);
+      const int gy = min(y0 + ty, p.ny - 1);
+      const double h = __ldg(hp + (size_t)gy * p.nx + gx);
+      v[r] = f ? -h : h;
+    } else if (idx < G::NX + G::NY) {  // H_y: row c of the y-extended tile, column tx
+      const int j = idx - G::NX, c = j >> 5, tx = j & 31;
+      int f;
+      const int gy = bmap_t<SYM>(y0 - M + c, p.ny, p.sym[1], f);
+      const int gx = min(x0 + tx, p.nx - 1);
+      const double h = __ldg(hp + FS + (size_t)gy * p.nx + gx);
+      v[r] = f ? -h : h;
+    }
+  }
+}
+
+template <int M, bool SYM>
+__global__ void __launch_bounds__(256, 4) divh_kernel(const KParams p,
+                                                      const double *__restrict__ H,
+                                                      double *__restrict__ qout,
+                                                      double *__restrict__ w,
+                                                      double *__restrict__ rout,
+                                                      unsigned int *__restrict__ flag, int zb,
+                                                      int ze) {
+  using G = DHGeom<M>;
+  __shared__ double sh[G::NX + G::NY];
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
+  const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 8;
+  const int x = x0 + tx, y = y0 + ty;
+  const bool valid = x < p.nx && y < p.ny;
+  const int z0 = zb + blockIdx.z * DH_Z;
+  const int nzo = min(DH_Z, ze - z0);
+  const size_t FS = (size_t)p.nx * p.ny;
+  const size_t off = (size_t)min(y, p.ny - 1) * p.nx + min(x, p.nx - 1);
+  // register window of H_z along z
+  double hz[DH_Z + 2 * M];
+#pragma unroll
+  for (int t = 0; t < DH_Z + 2 * M; ++t) {
+    hz[t] = 0.0;
+    if (t < nzo + 2 * M) {
+      int f;
+      const int zz = zread(p, z0 - M + t, f);
+      const double v = __ldg(H + (size_t)zz * 3 * FS + 2 * FS + off);
+      hz[t] = f ? -v : v;
+    }
+  }
+  double nxt[G::PER];
+  divh_fetch<M, SYM>(p, H, z0, x0, y0, tid, nxt);
+  bool bad = false;
+#pragma unroll
+  for (int j = 0; j < DH_Z; ++j) {
+    if (j >= nzo) break;
+    const int z = z0 + j;
+    // this plane's read-modify-write operands, in flight during the staging below
+    const size_t o = (size_t)z * 5 * FS + 4 * FS + off;
+    double *qe = qout ? qout + qplane(p, z) + 4 * FS + off : nullptr;
+    double q_old = 0.0, w_old = 0.0;
+    if (valid && !rout) {
+      q_old = *qe;
+      if (p.write_w) w_old = w[o];
+    }
+    __syncthreads();  // the previous plane's reads are done
+#pragma unroll
+    for (int r = 0; r < G::PER; ++r) {
+      const int idx = tid + 256 * r;
+      if (idx < G::NX + G::NY) sh[idx] = nxt[r];
+    }
+    __syncthreads();
+    if (j + 1 < nzo) divh_fetch<M, SYM>(p, H, z + 1, x0, y0, tid, nxt);
+    const double *rx = sh + ty * G::XW + tx + M;
+    const double *cy = sh + G::NX + (ty + M) * 32 + tx;
+    double sx = 0.0, sy = 0.0, sz = 0.0;
+#pragma unroll
+    for (int k = 1; k <= M; ++k) {
+      sx = fma(p.a[k - 1], rx[k] - rx[-k], sx);
+      sy = fma(p.a[k - 1], cy[32 * k] - cy[-32 * k], sy);
+      sz = fma(p.a[k - 1], hz[j + M + k] - hz[j + M - k], sz);
+    }
+    if (!valid) continue;
+    const double d = sx + sy + sz;
+    if (rout) {
+      rout[o] += d;
+      continue;
+    }
+    const double dd = p.dt * d;
+    const double qn = fma(p.B, dd, q_old);
+    *qe = qn;
+    bad |= !isfinite(qn);
+    if (p.write_w) w[o] = fma(p.two_reg ? p.beta : 1.0, dd, w_old);
+  }
+  if (bad) atomicOr(flag, 1u);
+}
+
+// cudaFuncSetAttribute (dynamic shared memory above 48 KB) once per kernel and
+// device: `done` holds one bit per device id (handles on several devices may
+// share a process; a lost race only repeats the call)
+template <typename K>
+cudaError_t ensure_smem_attr(K kern, int smem, unsigned &done) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const unsigned bit = 1u << (dev & 31);
+  if (done & bit) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e == cudaSuccess) done |= bit;
+  return e;
+}
+
+template <int M>
+cudaError_t zpass_launch(const KParams &p, const double *q, double *w, double *gz, int zb, int ze,
+                         int zb1, int ze1, cudaStream_t s) {
+  constexpr int smem = zp_smem_bytes<M>();
+  // symmetry in z (one GPU only) gets its own instantiation: mirrored plane reads
+  const int sz = (p.visc || p.cons) ? 2 : (p.zwrap && p.sym[2] ? 1 : 0);
+  auto kern = sz == 2 ? zpass_kernel<M, 2> : sz == 1 ? zpass_kernel<M, 1> : zpass_kernel<M, 0>;
+  static unsigned done[3] = {0, 0, 0};
+  cudaError_t e = ensure_smem_attr(kern, smem, done[sz]);
+  if (e != cudaSuccess) return e;
+  const int gx = (p.nx + ZP_TX - 1) / ZP_TX, gy = p.ny;
+  const int len = (ze - zb) > (ze1 - zb1) ? (ze - zb) : (ze1 - zb1);
+  const int chunks = (len + ZP_TZ - 1) / ZP_TZ;
+  // split the z-range into segments only when the pencils alone do not fill ~2 waves
+  int nseg = (2 * 148 + gx * gy - 1) / (gx * gy);
+  nseg = nseg < 1 ? 1 : (nseg > chunks ? chunks : nseg);
+  ZRange zr;
+  zr.seg_len = ((chunks + nseg - 1) / nseg) * ZP_TZ;
+  zr.b0 = zb;
+  zr.e0 = ze;
+  zr.nseg0 = (ze - zb + zr.seg_len - 1) / zr.seg_len;
+  zr.b1 = zb1;
+  zr.e1 = ze1 > zb1 ? ze1 : zb1;
+  const int nseg1 = (zr.e1 - zr.b1 + zr.seg_len - 1) / zr.seg_len;
+  dim3 grid(gx * gy, 1, zr.nseg0 + nseg1);
+  kern<<<grid, ZP_THREADS, smem, s>>>(p, q, w, gz, zr);
+  return cudaGetLastError();
+}
+
+template <int M>
+cudaError_t xypass_launch(const KParams &p, const double *q, double *qout, double *w,
+                          const double *gz, double *rout, unsigned int *flag, int zb, int ze,
+                          cudaStream_t s) {
+  constexpr int smem = ws::xy_smem_bytes<M>();
+  const int v = (p.visc || p.cons) ? 4 : (p.two_reg ? 1 : 0) + (p.sym[0] || p.sym[1] ? 2 : 0);
+  auto kern = v == 0   ? ws::xypass_kernel<M, 0>
+              : v == 1 ? ws::xypass_kernel<M, 1>
+              : v == 2 ? ws::xypass_kernel<M, 2>
+              : v == 3 ? ws::xypass_kernel<M, 3>
+                       : ws::xypass_kernel<M, 4>;
+  static unsigned done[5] = {0, 0, 0, 0, 0};
+  cudaError_t e = ensure_smem_attr(kern, smem, done[v]);
+  if (e != cudaSuccess) return e;
+  // planes per CTA: XY_SEG, halved while the grid would not cover the SMs (small grids)
+  const int tiles = ((p.nx + ws::XY_TX - 1) / ws::XY_TX) * ((p.ny + ws::XY_TY - 1) / ws::XY_TY);
+  int seg = ze - zb < ws::XY_SEG ? ze - zb : ws::XY_SEG;
+  while (seg > 1 && tiles * ((ze - zb + seg - 1) / seg) < 148) seg = (seg + 1) / 2;
+  dim3 grid((p.nx + ws::XY_TX - 1) / ws::XY_TX, (p.ny + ws::XY_TY - 1) / ws::XY_TY,
+            (ze - zb + seg - 1) / seg);
+  kern<<<grid, ws::XY_CTA, smem, s>>>(p, q, qout, w, gz, rout, flag, zb, ze, seg);
+  return cudaGetLastError();
+}
+
+template <int M>
+cudaError_t diag_launch(const KParams &p, const double *q, double *tpart, cudaStream_t s) {
+  const dim3 grid((p.nx + 31) / 32, (p.ny + DG_TY - 1) / DG_TY, (p.nz + DG_Z - 1) / DG_Z);
+  diag_kernel<M><<<grid, dim3(32, DG_TY), 0, s>>>(p, q, tpart, (int)(grid.x * grid.y));
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+namespace detail {
+template <>
+cudaError_t zpass_m<OSBLI_M>(const KParams &p, const double *q, double *w, double *gz, int zb,
+                             int ze, int zb1, int ze1, cudaStream_t s) {
+  return zpass_launch<OSBLI_M>(p, q, w, gz, zb, ze, zb1, ze1, s);
+}
+
+template <>
+cudaError_t xypass_m<OSBLI_M>(const KParams &p, const double *q, double *qout, double *w,
+                              const double *gz, double *rout, unsigned int *flag, int zb, int ze,
+                              cudaStream_t s) {
+  return xypass_launch<OSBLI_M>(p, q, qout, w, gz, rout, flag, zb, ze, s);
+}
+
+template <>
+cudaError_t divh_m<OSBLI_M>(const KParams &p, double *q_out, double *w, double *r_out,
+                            unsigned int *flag, int zb, int ze, cudaStream_t s) {
+  const dim3 grid((p.nx + 31) / 32, (p.ny + 7) / 8, (ze - zb + DH_Z - 1) / DH_Z);
+  const dim3 block(32, 8);
+  if (p.sym[0] || p.sym[1])
+    divh_kernel<OSBLI_M, true><<<grid, block, 0, s>>>(p, p.hflux, q_out, w, r_out, flag, zb, ze);
+  else
+    divh_kernel<OSBLI_M, false><<<grid, block, 0, s>>>(p, p.hflux, q_out, w, r_out, flag, zb, ze);
+  return cudaGetLastError();
+}
+
+template <>
+cudaError_t diag_m<OSBLI_M>(const KParams &p, const double *q, double *tpart, cudaStream_t s) {
+  return diag_launch<OSBLI_M>(p, q, tpart, s);
+}
+
+}  // namespace detail
+}  // namespace osbli

@@ -89,6 +89,7 @@ def load():
     L.osbli_loopback_step.argtypes = [ctypes.POINTER(H), c_int, c_int]
     L.osbli_set_source.argtypes = [H, vp, c_int]
     L.osbli_set_boundary.argtypes = [H, c_int, c_int]
+    L.osbli_set_slab_schedule.argtypes = [H, c_int]
     L.osbli_set_state_async.argtypes = [H, vp, c_int]
     L.osbli_get_state_async.argtypes = [H, vp, c_int]
     L.osbli_set_viscosity.argtypes = [H, c_int, ctypes.c_double]
@@ -245,6 +246,10 @@ class Solver:
 
     def sync(self):
         self._check(self._L.osbli_sync(self._h))
+
+    def set_slab_schedule(self, boundary_first: bool):
+        """Slab handles: boundary-first (True) or plain (False) stage schedule."""
+        self._check(self._L.osbli_set_slab_schedule(self._h, int(bool(boundary_first))))
 
     def set_boundary(self, direction: int, bc: int):
         """OSBLI_BC_PERIODIC or OSBLI_BC_SYMMETRY for direction 0/1/2."""

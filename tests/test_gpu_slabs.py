@@ -22,10 +22,13 @@ def osbli():
     return pkg
 
 
+@pytest.mark.parametrize("schedule", [0, 1])
 @pytest.mark.parametrize("order,nslabs,shape", [(4, 2, (24, 20, 16)), (4, 3, (24, 20, 17)),
                                                 (12, 2, (20, 18, 24)), (12, 4, (33, 17, 26)),
-                                                (8, 8, (16, 16, 64))])
-def test_loopback_slabs_bitwise_equal_single_domain(osbli, order, nslabs, shape):
+                                                (8, 8, (16, 16, 64)), (12, 2, (64, 48, 80))])
+def test_loopback_slabs_bitwise_equal_single_domain(osbli, order, nslabs, shape, schedule):
+    """Both stage schedules (plain; boundary first: interior z-pass, then the two
+    face ranges in one launch) on 2-8 slabs, uneven splits included."""
     dx = 2 * math.pi / max(shape)
     dt = 2e-3
     Q = perturbed_tgv(*shape, dx=dx, amp=0.02)
@@ -33,6 +36,8 @@ def test_loopback_slabs_bitwise_equal_single_domain(osbli, order, nslabs, shape)
     ref.set_state(Q)
     ref.step(3)
     grp = osbli.LoopbackGroup(*shape, order, dx, dt, nslabs, **TGV_PHYS)
+    for sl in grp.slabs:
+        sl.set_slab_schedule(schedule)
     grp.set_state(Q)
     assert [s.z0 for s in grp.slabs] == [osbli.slab_bounds(shape[2], nslabs, r)[0]
                                          for r in range(nslabs)]
@@ -94,9 +99,10 @@ def test_loopback_switch_combinations(osbli, scheme, visc, nslabs, order):
     grp.close()
 
 
+@pytest.mark.parametrize("schedule", [0, 1])
 @pytest.mark.parametrize("order,symz,cons", [(4, False, False), (12, False, False),
                                              (8, True, False), (6, False, True)])
-def test_single_rank_nccl_path_bitwise(osbli, order, symz, cons):
+def test_single_rank_nccl_path_bitwise(osbli, order, symz, cons, schedule):
     """One rank with an NCCL unique id runs the distributed code path with NCCL:
     its ghost planes come from itself through ncclSend/ncclRecv (or the mirror),
     the z-pass reads ghost planes, the diagnostics go through ncclAllGather.
@@ -107,6 +113,7 @@ def test_single_rank_nccl_path_bitwise(osbli, order, symz, cons):
     Q = perturbed_tgv(*shape, dx=dx, amp=0.05)
     uid = osbli.nccl_unique_id()
     dist = osbli.Solver(*shape, order, dx, dt, rank=0, nranks=1, unique_id=uid, **TGV_PHYS)
+    dist.set_slab_schedule(schedule)  # 1: exchange on the comm stream behind the interior z-pass
     ref = osbli.Solver(*shape, order, dx, dt, **TGV_PHYS)
     for s in (dist, ref):
         if symz:
@@ -121,3 +128,43 @@ def test_single_rank_nccl_path_bitwise(osbli, order, symz, cons):
         (d2.kinetic_energy, d2.enstrophy, d2.dissipation)
     if not cons:
         assert np.array_equal(dist.residual(), ref.residual())
+
+
+def test_loopback_nonfinite_is_agreed_by_every_slab(osbli):
+    """A non-finite value in one slab poisons every member of the group (the
+    collective flag policy of osbli_diagnostics / osbli_sync): none of them may
+    step again, so no slab waits on a peer that refuses."""
+    shape, order = (16, 12, 24), 4
+    Q = perturbed_tgv(*shape, dx=0.3, amp=0.02)
+    Q[0, 20, 3, 4] = 0.0  # rho = 0 in the last slab
+    grp = osbli.LoopbackGroup(*shape, order, 0.3, 1e-3, 3, **TGV_PHYS)
+    grp.set_state(Q)
+    grp.step(1)
+    with pytest.raises(osbli.OsbliError) as ei:
+        grp.slabs[0].diagnostics()
+    assert ei.value.status == "E_NONFINITE"
+    for sl in grp.slabs:
+        with pytest.raises(osbli.OsbliError) as ei:
+            sl.sync()
+        assert ei.value.status == "E_STATE"
+    with pytest.raises(osbli.OsbliError):
+        grp.step(1)
+    assert np.isfinite(grp.slabs[0].get_state()).any()  # get_state stays valid
+    grp.close()
+
+
+def test_loopback_member_destroyed_is_reported_not_crashed(osbli):
+    """Destroying one member breaks the group: the others report E_STATE from
+    calls that need the siblings instead of dereferencing the destroyed one."""
+    shape, order = (16, 12, 24), 4
+    grp = osbli.LoopbackGroup(*shape, order, 0.3, 1e-3, 3, **TGV_PHYS)
+    grp.set_state(perturbed_tgv(*shape, dx=0.3, amp=0.02))
+    grp.slabs[1].close()
+    for r in (0, 2):
+        with pytest.raises(osbli.OsbliError) as ei:
+            grp.slabs[r].diagnostics()
+        assert ei.value.status == "E_STATE"
+        with pytest.raises(osbli.OsbliError) as ei:
+            grp.slabs[r].residual()
+        assert ei.value.status == "E_STATE"
+    grp.close()
