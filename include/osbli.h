@@ -153,13 +153,19 @@ int osbli_create_loopback(int nx, int ny, int nz, int order, double dx, double d
 int osbli_loopback_step(osbli_ctx **hs, int nslabs, int n);
 
 /* Stage schedule of a slab handle (halo exchange per stage, P:141,
- * P:149): 0 = plain (exchange the ghost planes, then the z-pass and xy-pass over
- * the slab), 1 = boundary first (the exchange runs on a second stream behind the
- * interior z-pass; the z-pass of the 2m face planes follows it).  Default: 1 when
- * the slab has neighbours (nranks > 1 or a loopback group), 0 for one rank;
- * the environment variable OSBLI_SLAB_OVERLAP=0/1 read at create time overrides
- * the default.  No effect on single-domain handles; INVAL for other values. */
-int osbli_set_slab_schedule(osbli_ctx *h, int boundary_first);
+ * P:149).  Only the m planes next to each slab face need the neighbours' planes:
+ *   OSBLI_SLAB_PLAIN   exchange the ghost planes, then the z-pass and the xy-pass;
+ *   OSBLI_SLAB_ZSPLIT  the exchange runs on a second stream behind the interior
+ *                      z-pass; the z-pass of the 2m face planes follows it;
+ *   OSBLI_SLAB_XYSPLIT the xy-pass writes the face planes of the new state first;
+ *                      their exchange runs behind the interior xy-pass and the
+ *                      next stage waits for it.
+ * Default: XYSPLIT when the slab has neighbours (nranks > 1 or a loopback group),
+ * PLAIN for one rank; OSBLI_SLAB_OVERLAP=0/1/2 in the environment at create time
+ * overrides the default.  Results are bitwise the same in every schedule.  No
+ * effect on single-domain handles; INVAL for other values. */
+enum { OSBLI_SLAB_PLAIN = 0, OSBLI_SLAB_ZSPLIT = 1, OSBLI_SLAB_XYSPLIT = 2 };
+int osbli_set_slab_schedule(osbli_ctx *h, int schedule);
 
 /* Slab owned by this rank: global planes [*z0, *z0 + *nz_local). */
 int osbli_local_box(const osbli_ctx *h, int *z0, int *nz_local);

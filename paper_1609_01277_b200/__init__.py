@@ -18,6 +18,9 @@ from .native import (  # noqa: F401
     OSBLI_EULER,
     OSBLI_RK3,
     OSBLI_RK3_2R,
+    OSBLI_SLAB_PLAIN,
+    OSBLI_SLAB_XYSPLIT,
+    OSBLI_SLAB_ZSPLIT,
     LoopbackGroup,
     OsbliError,
     ScalarSolver,

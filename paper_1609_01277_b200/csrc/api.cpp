@@ -37,7 +37,9 @@ struct osbli_ctx {
   int nx = 0, ny = 0, nz_global = 0, nz = 0, z0 = 0, order = 0, m = 0, scheme = 0;
   int rank = 0, nranks = 1;
   bool slab = false;  // distributed (ghost-plane) path: nranks > 1, or one rank over NCCL
-  bool overlap = false;  // boundary-first split schedule (OSBLI_SLAB_OVERLAP=1)
+  // slab stage schedule (osbli_set_slab_schedule): OSBLI_SLAB_PLAIN, _ZSPLIT, _XYSPLIT
+  int overlap = 0;
+  bool ghost_async = false;  // the ghost planes of the current Q were posted on comm_stream
   double dx = 0, dt = 0, Re = 0, Pr = 0, Minf = 0, gamma = 0;
   int device = 0;
   cudaStream_t stream = nullptr, own_stream = nullptr;
@@ -225,11 +227,10 @@ void slab_partition(int nz, int nranks, int rank, int *z0, int *nzl) {
 // schedule; by default the boundary-first one runs whenever the ghost planes come
 // from other slabs (nslabs > 1), the plain one for a single rank exchanging with
 // itself.  osbli_set_slab_schedule overrides either.
-bool slab_overlap_from_env(int nslabs) {
+int slab_overlap_from_env(int nslabs) {
   const char *v = std::getenv("OSBLI_SLAB_OVERLAP");
-  if (v && v[0] == '1') return true;
-  if (v && v[0] == '0') return false;
-  return nslabs > 1;
+  if (v && v[0] >= '0' && v[0] <= '2' && v[1] == 0) return v[0] - '0';
+  return nslabs > 1 ? OSBLI_SLAB_XYSPLIT : OSBLI_SLAB_PLAIN;
 }
 
 void ghost_plan(int rank, int nranks, int nzl, int m, int plan[8], bool symz = false) {
@@ -296,6 +297,18 @@ int exchange_planes(osbli_ctx *h, double *base, int nf, int odd, Sibling sibling
 // ghost planes of the current state Q (buffer q = h->b.q[h->cur])
 int exchange_ghosts(osbli_ctx *h, double *q, cudaStream_t st = nullptr) {
   return exchange_planes(h, q, 5, 3, [](osbli_ctx *s) { return s->b.q[s->cur]; }, st);
+}
+
+// ghost planes of the current Q valid in stream order on h->stream: wait for the
+// exchange the previous stage posted on the comm stream (xy-split schedule), or
+// exchange now
+int current_ghosts(osbli_ctx *h) {
+  if (h->ghost_async) {
+    CK(h, cudaStreamWaitEvent(h->stream, h->ev_ghost, 0));
+    h->ghost_async = false;
+    return OSBLI_OK;
+  }
+  return exchange_ghosts(h, h->b.q[h->cur], h->stream);
 }
 
 // ghost planes of the viscous-work flux H_j (conservative form, D-27): the
@@ -466,6 +479,7 @@ static int set_state_impl(osbli_ctx *h, const double *q, int on_device, bool syn
                         on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, h->stream));
   CK(h, osbli::launch_abi_to_internal(h->base, stage, h->b.q[h->cur], h->stream, &h->launches));
   if (h->ev_qready) CK(h, cudaEventRecord(h->ev_qready, h->stream));
+  h->ghost_async = false;
   CK(h, cudaMemsetAsync(h->b.flag, 0, sizeof(unsigned int), h->stream));
   if (sync) CK(h, cudaStreamSynchronize(h->stream));
   h->step_count = 0;
@@ -557,56 +571,67 @@ int run_stage(osbli_ctx *h, int s, bool exchange = true, bool divh = true) {
     h->cur ^= 1;
     return OSBLI_OK;
   }
-  if (!h->overlap) {
-    // Slab decomposition, plain schedule: exchange the ghost planes, then one
-    // z-pass and one xy-pass over the whole slab.  (At 256^2 planes the exchange
-    // is ~30 MB per stage; the split schedule below hides it but costs more in
-    // its six small launches than it saves.)
-    if (h->comm) {
-      int r = exchange_ghosts(h, qin, h->stream);
-      if (r) return r;
-    } else if (exchange) {
-      int r = exchange_ghosts(h, qin);
-      if (r) return r;
-    }
-    if (ev) CK(h, cudaEventRecord(ev[0], h->stream));
-    CK(h, osbli::launch_zpass(p, qin, wz, h->b.gz, 0, h->nz, h->stream, &h->launches));
-    if (ev) CK(h, cudaEventRecord(ev[1], h->stream));
-    CK(h, osbli::launch_xypass(p, qin, qout, h->b.w, h->b.gz, nullptr, h->b.flag, 0, h->nz,
-                               h->stream, &h->launches));
-    if (ev) CK(h, cudaEventRecord(ev[2], h->stream));
-    if (p.cons && divh) {
-      int r = exchange_hflux(h, h->stream);
-      if (r) return r;
-      CK(h, osbli::launch_divh(p, qout, h->b.w, nullptr, h->b.flag, 0, h->nz, h->stream,
-                               &h->launches));
-    }
-    h->cur ^= 1;
-    return OSBLI_OK;
-  }
-  // Slab decomposition, boundary first: only the z-pass of the m
-  // planes next to each slab face reads ghost planes.  The exchange of Q's
-  // boundary planes runs on the comm stream while the interior z-pass runs; the
-  // z-pass of the 2m face planes (one launch, two ranges) waits for it; the
-  // xy-pass (no z taps) runs over the whole slab.  3 launches per stage instead
-  // of 2; the exchange hides behind nz - 2m planes of z-pass.
+  // Slab decomposition.  The m planes next to each slab face are
+  // the only ones whose z-pass reads ghost planes and the only ones the
+  // neighbours read.  Three schedules:
+  //   PLAIN   exchange; z-pass; xy-pass                                 (2 launches)
+  //   ZSPLIT  exchange on the comm stream || interior z-pass; face z-pass (both
+  //           faces, one launch); xy-pass                               (3 launches)
+  //   XYSPLIT z-pass; face xy-pass (both faces, one launch); exchange of the NEW
+  //           state's faces on the comm stream || interior xy-pass; the next
+  //           stage's z-pass waits for it                             (3 launches)
+  // (the conservative viscous work finishes Q' only after its divergence kernel:
+  // it keeps the plain order after the xy-pass)
   const int m = h->m;
   const int lo = m < h->nz ? m : h->nz;            // [0, lo): low face planes
   const int hi = h->nz - m > lo ? h->nz - m : lo;  // [hi, nz): high face planes
-  if (h->comm) {
+  const int mode = h->overlap;
+  // ---- ghost planes of Q (qin)
+  if (h->comm && mode == OSBLI_SLAB_ZSPLIT && !h->ghost_async) {
     CK(h, cudaStreamWaitEvent(h->comm_stream, h->ev_qready, 0));
     int r = exchange_ghosts(h, qin, h->comm_stream);
     if (r) return r;
     CK(h, cudaEventRecord(h->ev_ghost, h->comm_stream));
+    h->ghost_async = true;
+  } else if (h->comm) {
+    int r = current_ghosts(h);
+    if (r) return r;
   } else if (exchange) {
     int r = exchange_ghosts(h, qin);
     if (r) return r;
   }
+  // ---- z-pass
   if (ev) CK(h, cudaEventRecord(ev[0], h->stream));
-  CK(h, osbli::launch_zpass(p, qin, wz, h->b.gz, lo, hi, h->stream, &h->launches));
-  if (h->comm) CK(h, cudaStreamWaitEvent(h->stream, h->ev_ghost, 0));
-  CK(h, osbli::launch_zpass(p, qin, wz, h->b.gz, 0, lo, h->stream, &h->launches, hi, h->nz));
+  if (mode == OSBLI_SLAB_ZSPLIT) {
+    CK(h, osbli::launch_zpass(p, qin, wz, h->b.gz, lo, hi, h->stream, &h->launches));
+    if (h->ghost_async) {
+      CK(h, cudaStreamWaitEvent(h->stream, h->ev_ghost, 0));
+      h->ghost_async = false;
+    }
+    CK(h, osbli::launch_zpass(p, qin, wz, h->b.gz, 0, lo, h->stream, &h->launches, hi, h->nz));
+  } else {
+    CK(h, osbli::launch_zpass(p, qin, wz, h->b.gz, 0, h->nz, h->stream, &h->launches));
+  }
   if (ev) CK(h, cudaEventRecord(ev[1], h->stream));
+  // ---- xy-pass
+  if (mode == OSBLI_SLAB_XYSPLIT && !p.cons) {
+    CK(h, osbli::launch_xypass(p, qin, qout, h->b.w, h->b.gz, nullptr, h->b.flag, 0, lo,
+                               h->stream, &h->launches, hi, h->nz));
+    if (h->comm) {
+      // the faces of Q' are final: their exchange runs behind the interior xy-pass
+      CK(h, cudaEventRecord(h->ev_qready, h->stream));
+      CK(h, cudaStreamWaitEvent(h->comm_stream, h->ev_qready, 0));
+      int r = exchange_ghosts(h, qout, h->comm_stream);
+      if (r) return r;
+      CK(h, cudaEventRecord(h->ev_ghost, h->comm_stream));
+    }
+    CK(h, osbli::launch_xypass(p, qin, qout, h->b.w, h->b.gz, nullptr, h->b.flag, lo, hi,
+                               h->stream, &h->launches));
+    if (ev) CK(h, cudaEventRecord(ev[2], h->stream));
+    h->cur ^= 1;
+    h->ghost_async = h->comm != nullptr;  // ghosts of the new current Q are in flight
+    return OSBLI_OK;
+  }
   CK(h, osbli::launch_xypass(p, qin, qout, h->b.w, h->b.gz, nullptr, h->b.flag, 0, h->nz,
                              h->stream, &h->launches));
   if (ev) CK(h, cudaEventRecord(ev[2], h->stream));
@@ -763,14 +788,12 @@ int osbli_loopback_step(osbli_ctx **hs, int nslabs, int n) {
   return OSBLI_OK;
 }
 
-int osbli_set_slab_schedule(osbli_ctx *h, int boundary_first) {
+int osbli_set_slab_schedule(osbli_ctx *h, int schedule) {
   int u = check_usable(h);
   if (u) return u;
-  if (boundary_first != 0 && boundary_first != 1) return fail(h, OSBLI_E_INVAL, "schedule must be 0 or 1");
-  if (h->slab) {
-    CK(h, cudaStreamSynchronize(h->stream));
-    h->overlap = boundary_first != 0;
-  }
+  if (schedule < OSBLI_SLAB_PLAIN || schedule > OSBLI_SLAB_XYSPLIT)
+    return fail(h, OSBLI_E_INVAL, "schedule must be OSBLI_SLAB_PLAIN, _ZSPLIT or _XYSPLIT");
+  if (h->slab) h->overlap = schedule;
   return OSBLI_OK;
 }
 
@@ -854,7 +877,7 @@ int osbli_residual(osbli_ctx *h, double *R, int on_device) {
                 "the residual hook of a slab handle has no viscous-work flux exchange");
   const size_t n = (size_t)5 * h->nz * h->nx * h->ny;
   double *qin = h->b.q[h->cur];
-  int r = exchange_ghosts(h, qin);
+  int r = h->comm ? current_ghosts(h) : exchange_ghosts(h, qin);
   if (r) return r;
   // R lands in W ([nz][5] plane-major: A = 0, dt = 1 so that W' = Rz and R = W' + R_xy),
   // then is transposed into the idle ping-pong buffer (ABI layout)
@@ -899,7 +922,7 @@ int osbli_diagnostics(osbli_ctx *h, osbli_diag *out) {
     }
   } else {
     double *qin = h->b.q[h->cur];
-    r = exchange_ghosts(h, qin);
+    r = h->comm ? current_ghosts(h) : exchange_ghosts(h, qin);
     if (r) return r;
     CK(h, osbli::launch_diagnostics(h->base, qin, h->scratch, h->b.diag_part, h->stream,
                                     &h->launches));

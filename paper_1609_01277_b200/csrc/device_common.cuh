@@ -51,6 +51,32 @@ __device__ __forceinline__ int bmap(int i, int n, int sym, int &flip) {
   return flip ? 2 * n - 1 - c : c;
 }
 
+// The planes of one launch: segments of seg_len planes of [b0, e0) (blockIdx.z <
+// nseg0), then of [b1, e1) (the face planes at both ends of a slab in one launch,
+// DESIGN.md §6); b1 = e1 for a single range.
+struct PlaneRange {
+  int b0, e0, nseg0, b1, e1, seg_len;
+  // this CTA's planes [zs, ze); false when empty
+  __device__ __forceinline__ bool segment(int &zs, int &ze) const {
+    const bool r1 = (int)blockIdx.z >= nseg0;
+    zs = (r1 ? b1 : b0) + (int)(r1 ? blockIdx.z - nseg0 : blockIdx.z) * seg_len;
+    ze = min(r1 ? e1 : e0, zs + seg_len);
+    return zs < ze;
+  }
+};
+
+inline PlaneRange plane_range(int zb, int ze, int zb1, int ze1, int seg_len, int *nseg_total) {
+  PlaneRange r;
+  r.seg_len = seg_len;
+  r.b0 = zb;
+  r.e0 = ze;
+  r.nseg0 = (ze - zb + seg_len - 1) / seg_len;
+  r.b1 = zb1;
+  r.e1 = ze1 > zb1 ? ze1 : zb1;
+  *nseg_total = r.nseg0 + (r.e1 - r.b1 + seg_len - 1) / seg_len;
+  return r;
+}
+
 __device__ __forceinline__ size_t qplane(const KParams &p, int z) {
   return (size_t)(z + p.G) * 5 * (size_t)p.nx * p.ny;
 }

@@ -17,7 +17,8 @@ cudaError_t zpass_m(const KParams &p, const double *q, double *w, double *gz, in
                     int zb1, int ze1, cudaStream_t s);
 template <int M>
 cudaError_t xypass_m(const KParams &p, const double *q, double *qout, double *w, const double *gz,
-                     double *rout, unsigned int *flag, int zb, int ze, cudaStream_t s);
+                     double *rout, unsigned int *flag, int zb, int ze, int zb1, int ze1,
+                     cudaStream_t s);
 template <int M>
 cudaError_t divh_m(const KParams &p, double *q_out, double *w, double *r_out, unsigned int *flag,
                    int zb, int ze, cudaStream_t s);

@@ -127,10 +127,15 @@ cudaError_t launch_zpass(const KParams &p, const double *q_in, double *w, double
 
 cudaError_t launch_xypass(const KParams &p, const double *q_in, double *q_out, double *w,
                           const double *gz, double *r_out, unsigned int *flag,
-                          int zb, int ze, cudaStream_t s, long long *launches) {
-  if (ze <= zb) return cudaSuccess;
+                          int zb, int ze, cudaStream_t s, long long *launches, int zb1, int ze1) {
+  if (ze <= zb) {  // only the second range (or nothing)
+    if (ze1 <= zb1) return cudaSuccess;
+    zb = zb1;
+    ze = ze1;
+    zb1 = ze1 = 0;
+  }
   ++*launches;
-  OSBLI_DISPATCH_M(p.m, xypass_m, p, q_in, q_out, w, gz, r_out, flag, zb, ze, s)
+  OSBLI_DISPATCH_M(p.m, xypass_m, p, q_in, q_out, w, gz, r_out, flag, zb, ze, zb1, ze1, s)
 }
 
 cudaError_t launch_divh(const KParams &p, double *q_out, double *w, double *r_out,

@@ -77,10 +77,11 @@ cudaError_t launch_mirror_planes(const KParams &p, double *base, int nf, int odd
 cudaError_t launch_zpass(const KParams &p, const double *q_in, double *w, double *gz,
                          int z_begin, int z_end, cudaStream_t s, long long *launches,
                          int z_begin1 = 0, int z_end1 = 0);
-// xy-pass restricted to planes [z_begin, z_end).
+// xy-pass restricted to planes [z_begin, z_end) and, in the same launch, [z_begin1, z_end1).
 cudaError_t launch_xypass(const KParams &p, const double *q_in, double *q_out, double *w,
                           const double *gz, double *r_out, unsigned int *flag, int z_begin,
-                          int z_end, cudaStream_t s, long long *launches);
+                          int z_end, cudaStream_t s, long long *launches, int z_begin1 = 0,
+                          int z_end1 = 0);
 
 // Per-plane diagnostics partial sums [nz][3] (E_k, enstrophy, dissipation sums).
 // scratch: >= diagnostics_scratch(p) doubles (per-(plane, tile) partials).

@@ -335,15 +335,9 @@ cudaError_t zpass_launch(const KParams &p, const double *q, double *w, double *g
   // split the z-range into segments only when the pencils alone do not fill ~2 waves
   int nseg = (2 * 148 + gx * gy - 1) / (gx * gy);
   nseg = nseg < 1 ? 1 : (nseg > chunks ? chunks : nseg);
-  ZRange zr;
-  zr.seg_len = ((chunks + nseg - 1) / nseg) * ZP_TZ;
-  zr.b0 = zb;
-  zr.e0 = ze;
-  zr.nseg0 = (ze - zb + zr.seg_len - 1) / zr.seg_len;
-  zr.b1 = zb1;
-  zr.e1 = ze1 > zb1 ? ze1 : zb1;
-  const int nseg1 = (zr.e1 - zr.b1 + zr.seg_len - 1) / zr.seg_len;
-  dim3 grid(gx * gy, 1, zr.nseg0 + nseg1);
+  int ntot = 0;
+  const PlaneRange zr = plane_range(zb, ze, zb1, ze1, ((chunks + nseg - 1) / nseg) * ZP_TZ, &ntot);
+  dim3 grid(gx * gy, 1, ntot);
   kern<<<grid, ZP_THREADS, smem, s>>>(p, q, w, gz, zr);
   return cudaGetLastError();
 }
@@ -351,7 +345,7 @@ cudaError_t zpass_launch(const KParams &p, const double *q, double *w, double *g
 template <int M>
 cudaError_t xypass_launch(const KParams &p, const double *q, double *qout, double *w,
                           const double *gz, double *rout, unsigned int *flag, int zb, int ze,
-                          cudaStream_t s) {
+                          int zb1, int ze1, cudaStream_t s) {
   constexpr int smem = ws::xy_smem_bytes<M>();
   const int v = (p.visc || p.cons) ? 4 : (p.two_reg ? 1 : 0) + (p.sym[0] || p.sym[1] ? 2 : 0);
   auto kern = v == 0   ? ws::xypass_kernel<M, 0>
@@ -364,11 +358,15 @@ cudaError_t xypass_launch(const KParams &p, const double *q, double *qout, doubl
   if (e != cudaSuccess) return e;
   // planes per CTA: XY_SEG, halved while the grid would not cover the SMs (small grids)
   const int tiles = ((p.nx + ws::XY_TX - 1) / ws::XY_TX) * ((p.ny + ws::XY_TY - 1) / ws::XY_TY);
-  int seg = ze - zb < ws::XY_SEG ? ze - zb : ws::XY_SEG;
-  while (seg > 1 && tiles * ((ze - zb + seg - 1) / seg) < 148) seg = (seg + 1) / 2;
-  dim3 grid((p.nx + ws::XY_TX - 1) / ws::XY_TX, (p.ny + ws::XY_TY - 1) / ws::XY_TY,
-            (ze - zb + seg - 1) / seg);
-  kern<<<grid, ws::XY_CTA, smem, s>>>(p, q, qout, w, gz, rout, flag, zb, ze, seg);
+  const int nz1 = ze1 > zb1 ? ze1 - zb1 : 0;
+  const int len = (ze - zb) > nz1 ? (ze - zb) : nz1;
+  int seg = len < ws::XY_SEG ? len : ws::XY_SEG;
+  auto ctas = [&](int sg) { return tiles * ((ze - zb + sg - 1) / sg + (nz1 + sg - 1) / sg); };
+  while (seg > 1 && ctas(seg) < 148) seg = (seg + 1) / 2;
+  int ntot = 0;
+  const PlaneRange zr = plane_range(zb, ze, zb1, ze1, seg, &ntot);
+  dim3 grid((p.nx + ws::XY_TX - 1) / ws::XY_TX, (p.ny + ws::XY_TY - 1) / ws::XY_TY, ntot);
+  kern<<<grid, ws::XY_CTA, smem, s>>>(p, q, qout, w, gz, rout, flag, zr);
   return cudaGetLastError();
 }
 
@@ -391,8 +389,8 @@ cudaError_t zpass_m<OSBLI_M>(const KParams &p, const double *q, double *w, doubl
 template <>
 cudaError_t xypass_m<OSBLI_M>(const KParams &p, const double *q, double *qout, double *w,
                               const double *gz, double *rout, unsigned int *flag, int zb, int ze,
-                              cudaStream_t s) {
-  return xypass_launch<OSBLI_M>(p, q, qout, w, gz, rout, flag, zb, ze, s);
+                              int zb1, int ze1, cudaStream_t s) {
+  return xypass_launch<OSBLI_M>(p, q, qout, w, gz, rout, flag, zb, ze, zb1, ze1, s);
 }
 
 template <>

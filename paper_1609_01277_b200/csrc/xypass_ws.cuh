@@ -344,7 +344,7 @@ __global__ void __launch_bounds__(XY_CTA, 1)
     xypass_kernel(const KParams p, const double *__restrict__ q, double *__restrict__ qout,
                   double *__restrict__ w, const double *__restrict__ gz,
                   double *__restrict__ rout,
-                  unsigned int *__restrict__ flag, int z_begin, int z_end, int seg_len) {
+                  unsigned int *__restrict__ flag, const PlaneRange zr) {
   // XF bits: 1 = two-register epilogue, 2 = symmetry in x/y, 4 = equation variants
   // (mu(T), conservative viscous work), which take the other two at run time
   constexpr bool VAR = (XF & 4) != 0;
@@ -360,9 +360,8 @@ __global__ void __launch_bounds__(XY_CTA, 1)
   XT = SM + Gm::OFF_XT;
   const int tid = threadIdx.x;
   const int x0 = blockIdx.x * XY_TX, y0 = blockIdx.y * XY_TY;
-  const int zs = z_begin + blockIdx.z * seg_len;
-  const int ze = min(z_end, zs + seg_len);
-  if (zs >= ze) return;
+  int zs, ze;
+  if (!zr.segment(zs, ze)) return;
   const size_t FS = (size_t)p.nx * p.ny;
   const int grp = tid >> 7;  // 0: velocity group A, 1: conservative group B (warp-uniform)
   const int q7 = tid & 127;

@@ -127,17 +127,10 @@ __device__ __forceinline__ double d2w(const KParams &p, const double (&v)[ZP_RZ 
 // ZF = 0: periodic z / ghost planes; 1: symmetry in z (mirrored plane reads);
 // 2: equation variants (mu(T), conservative viscous work; D-26, D-27) with
 // run-time boundary handling.  Separate instantiations keep the default path lean.
-// The planes of one launch: segments of seg_len planes of [b0, e0) (blockIdx.z <
-// nseg0), then of [b1, e1) (the boundary planes at both slab faces in one launch,
-// DESIGN.md §6); b1 = e1 for a single range.
-struct ZRange {
-  int b0, e0, nseg0, b1, e1, seg_len;
-};
-
 template <int M, int ZF>
 __global__ void __launch_bounds__(ZP_THREADS, OSBLI_ZP_MINB)
     zpass_kernel(const KParams p, const double *__restrict__ q, double *__restrict__ w,
-                 double *__restrict__ gz, const ZRange zr) {
+                 double *__restrict__ gz, const PlaneRange zr) {
   constexpr bool SYMZ = ZF != 0;
   constexpr bool VAR = ZF == 2;
   using Zg = ZGeom<M>;
@@ -148,10 +141,8 @@ __global__ void __launch_bounds__(ZP_THREADS, OSBLI_ZP_MINB)
   // blockIdx.x enumerates (x-tile, y-row) pencils (grid.y would cap ny at 65535)
   const int gx = (p.nx + ZP_TX - 1) / ZP_TX;
   const int x0 = (int)(blockIdx.x % gx) * ZP_TX, y = (int)(blockIdx.x / gx);
-  const bool r1 = (int)blockIdx.z >= zr.nseg0;
-  const int zs = (r1 ? zr.b1 : zr.b0) + (int)(r1 ? blockIdx.z - zr.nseg0 : blockIdx.z) * zr.seg_len;
-  const int ze = min(r1 ? zr.e1 : zr.e0, zs + zr.seg_len);
-  if (zs >= ze) return;
+  int zs, ze;
+  if (!zr.segment(zs, ze)) return;
   const int nchunks = (ze - zs + ZP_TZ - 1) / ZP_TZ;
   const size_t FS = (size_t)p.nx * p.ny;
   // column this thread loads for staging slot c = tid & 31 (ragged tiles load any valid column)

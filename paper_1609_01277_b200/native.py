@@ -24,6 +24,9 @@ OSBLI_VISC_CONSTANT = 0
 OSBLI_VISC_SUTHERLAND = 1
 OSBLI_ENERGY_EXPANDED = 0
 OSBLI_ENERGY_CONSERVATIVE = 1
+OSBLI_SLAB_PLAIN = 0
+OSBLI_SLAB_ZSPLIT = 1
+OSBLI_SLAB_XYSPLIT = 2
 _STATUS = {0: "OK", -1: "E_INVAL", -2: "E_UNSUPPORTED", -3: "E_NOMEM", -4: "E_CUDA",
            -5: "E_COMM", -6: "E_NONFINITE", -7: "E_STATE"}
 
@@ -247,9 +250,9 @@ class Solver:
     def sync(self):
         self._check(self._L.osbli_sync(self._h))
 
-    def set_slab_schedule(self, boundary_first: bool):
-        """Slab handles: boundary-first (True) or plain (False) stage schedule."""
-        self._check(self._L.osbli_set_slab_schedule(self._h, int(bool(boundary_first))))
+    def set_slab_schedule(self, schedule: int):
+        """Slab handles: OSBLI_SLAB_PLAIN (0), _ZSPLIT (1) or _XYSPLIT (2)."""
+        self._check(self._L.osbli_set_slab_schedule(self._h, int(schedule)))
 
     def set_boundary(self, direction: int, bc: int):
         """OSBLI_BC_PERIODIC or OSBLI_BC_SYMMETRY for direction 0/1/2."""

@@ -22,13 +22,14 @@ def osbli():
     return pkg
 
 
-@pytest.mark.parametrize("schedule", [0, 1])
+@pytest.mark.parametrize("schedule", [0, 1, 2])
 @pytest.mark.parametrize("order,nslabs,shape", [(4, 2, (24, 20, 16)), (4, 3, (24, 20, 17)),
                                                 (12, 2, (20, 18, 24)), (12, 4, (33, 17, 26)),
                                                 (8, 8, (16, 16, 64)), (12, 2, (64, 48, 80))])
 def test_loopback_slabs_bitwise_equal_single_domain(osbli, order, nslabs, shape, schedule):
-    """Both stage schedules (plain; boundary first: interior z-pass, then the two
-    face ranges in one launch) on 2-8 slabs, uneven splits included."""
+    """The three stage schedules (plain; z-split: interior z-pass, then the two
+    face ranges in one launch; xy-split: face xy-pass, then the interior one;
+    DESIGN.md §6) on 2-8 slabs, uneven splits included."""
     dx = 2 * math.pi / max(shape)
     dt = 2e-3
     Q = perturbed_tgv(*shape, dx=dx, amp=0.02)
@@ -99,7 +100,7 @@ def test_loopback_switch_combinations(osbli, scheme, visc, nslabs, order):
     grp.close()
 
 
-@pytest.mark.parametrize("schedule", [0, 1])
+@pytest.mark.parametrize("schedule", [0, 1, 2])
 @pytest.mark.parametrize("order,symz,cons", [(4, False, False), (12, False, False),
                                              (8, True, False), (6, False, True)])
 def test_single_rank_nccl_path_bitwise(osbli, order, symz, cons, schedule):
@@ -113,7 +114,9 @@ def test_single_rank_nccl_path_bitwise(osbli, order, symz, cons, schedule):
     Q = perturbed_tgv(*shape, dx=dx, amp=0.05)
     uid = osbli.nccl_unique_id()
     dist = osbli.Solver(*shape, order, dx, dt, rank=0, nranks=1, unique_id=uid, **TGV_PHYS)
-    dist.set_slab_schedule(schedule)  # 1: exchange on the comm stream behind the interior z-pass
+    # 1: exchange on the comm stream behind the interior z-pass; 2: the new state's
+    # faces exchanged behind the interior xy-pass, waited for by the next stage
+    dist.set_slab_schedule(schedule)
     ref = osbli.Solver(*shape, order, dx, dt, **TGV_PHYS)
     for s in (dist, ref):
         if symz:
