@@ -61,17 +61,24 @@ enum { XP_P = 0, XP_R = 1 };
 template <int M>
 struct XYGeom {
   static constexpr int HX = XY_TX + 2 * M;
-  static constexpr int PX = HX | 1;         // odd pitch (doubles): conflict-free row-per-lane access
+  // Even m (orders 4, 8, 12): the halo row starts at an even x, so it is copied in
+  // 16-byte pairs and the x-windows are read with 16-byte loads; a pitch of 2 mod 4
+  // doubles keeps those loads conflict-free for the row-per-lane access of phase X
+  // (8 lanes of a quarter warp on 8 rows hit 8 distinct 16-byte bank groups).
+  // Odd m: an odd pitch keeps the 8-byte row-per-lane loads conflict-free.
+  static constexpr bool PAIRS = (M % 2) == 0;
+  static constexpr int PX = PAIRS ? ((HX % 4 == 0) ? HX + 2 : HX) : (HX | 1);
   static constexpr int HY = XY_TY + 2 * M;
   static constexpr int FSZ = HY * PX;       // one full-halo field
   static constexpr int TP = XY_TX + 1;      // odd row pitch of tile-column arrays
   static constexpr int NPT = TP * XY_TY;    // tile points (padded)
   static constexpr int EXT = TP * HY;       // tile columns x (tile + y-halo) rows
   static constexpr int W = 4 + 2 * M;       // window length (RX = RY = 4)
-  // plane buffer (doubles): 6 full-halo fields | g02 [TY][PX] (tile rows) | g12 [HY][TP] (tile cols)
+  static constexpr int GP = XY_TX;          // pitch of the g12 strip (column-per-lane access)
+  // plane buffer (doubles): 6 full-halo fields | g02 [TY][PX] (tile rows) | g12 [HY][GP] (tile cols)
   static constexpr int PB_G02 = XF_N * FSZ;
   static constexpr int PB_G12 = PB_G02 + XY_TY * PX;
-  static constexpr int PBSZ = PB_G12 + EXT;
+  static constexpr int PBSZ = PB_G12 + HY * GP;
   // layout: PB[2] | PR (p, r) | E0 | E1 | XA[5] | XB[5] | XT
   static constexpr int OFF_PR = 2 * PBSZ;
   static constexpr int OFF_E0 = OFF_PR + 2 * FSZ;   // [HY][TP]   g00 (y-extended)
@@ -80,7 +87,9 @@ struct XYGeom {
   static constexpr int OFF_XB = OFF_XA + 5 * NPT;   // 5 x [TY][TP]
   static constexpr int OFF_XT = OFF_XB + 5 * NPT;   // [TY][TP] D_x T (equation variants)
   static constexpr int TOTAL = OFF_XT + NPT;
-  static constexpr int BYTES = TOTAL * (int)sizeof(double);
+  // producer gather tables (ints): global x of each halo column, y * nx of each halo row
+  static constexpr int TAB_INTS = HX + HY;
+  static constexpr int BYTES = TOTAL * (int)sizeof(double) + TAB_INTS * (int)sizeof(int);
 };
 
 template <int M>
@@ -92,11 +101,22 @@ constexpr int xy_smem_bytes() {
 // compiler may otherwise contract a product into the stencil difference
 // (f+ - f-) differently for different taps, and a uniform state would no
 // longer cancel exactly (SURVEY §8(c) equilibrium pin).
-// window of W values starting at base, stride `st` (doubles)
-template <int W>
+// window of W values starting at base, stride `st` (doubles); PAIR: consecutive
+// values (st = 1) from a 16-byte aligned base, read as W/2 16-byte loads
+template <int W, bool PAIR = false>
 __device__ __forceinline__ void ldwin(const double *base, int st, double (&v)[W]) {
+  if (PAIR) {
+    static_assert(W % 2 == 0, "pair windows need an even length");
 #pragma unroll
-  for (int k = 0; k < W; ++k) v[k] = base[k * st];
+    for (int k = 0; k < W / 2; ++k) {
+      const double2 t = reinterpret_cast<const double2 *>(base)[k];
+      v[2 * k] = t.x;
+      v[2 * k + 1] = t.y;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < W; ++k) v[k] = base[k * st];
+  }
 }
 
 template <int M, int W>
@@ -157,11 +177,12 @@ __device__ __forceinline__ void velocity_dir(const KParams &p, const double *S, 
                                              VelResult<M> &o) {
   using Gm = XYGeom<M>;
   constexpr int W = Gm::W;
+  constexpr bool PW = DIR == 0 && Gm::PAIRS;  // x-windows: 16-byte loads
   double r[W], v[W], t[W];
-  ldwin<W>(PR + XP_R * Gm::FSZ + base, st, r);
+  ldwin<W, PW>(PR + XP_R * Gm::FSZ + base, st, r);
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
-    ldwin<W>(S + (XF_M0 + i) * Gm::FSZ + base, st, t);
+    ldwin<W, PW>(S + (XF_M0 + i) * Gm::FSZ + base, st, t);
 #pragma unroll
     for (int k = 0; k < W; ++k) v[k] = __dmul_rn(t[k], r[k]);
 #pragma unroll
@@ -172,7 +193,7 @@ __device__ __forceinline__ void velocity_dir(const KParams &p, const double *S, 
     }
   }
   if (TW) {
-    ldwin<W>(PR + XP_P * Gm::FSZ + base, st, t);
+    ldwin<W, PW>(PR + XP_P * Gm::FSZ + base, st, t);
 #pragma unroll
     for (int k = 0; k < W; ++k) v[k] = __dmul_rn(__dmul_rn(p.gM2, t[k]), r[k]);
 #pragma unroll
@@ -182,10 +203,10 @@ __device__ __forceinline__ void velocity_dir(const KParams &p, const double *S, 
       o.Tc[j] = v[j + M];
     }
   }
-  ldwin<W>(S + XF_G22 * Gm::FSZ + base, st, v);  // D_d g22
+  ldwin<W, PW>(S + XF_G22 * Gm::FSZ + base, st, v);  // D_d g22
 #pragma unroll
   for (int j = 0; j < 4; ++j) o.mixA[j] = wd1<M, W>(p, v, j);
-  ldwin<W>(gmix, gst, v);  // DIR 0: D_x g02 = D_z g00 ; DIR 1: D_y g12 = D_z g11
+  ldwin<W, PW>(gmix, gst, v);  // DIR 0: D_x g02 = D_z g00 ; DIR 1: D_y g12 = D_z g11
 #pragma unroll
   for (int j = 0; j < 4; ++j) o.mixB[j] = wd1<M, W>(p, v, j);
   if (DIR == 1) {
@@ -209,19 +230,20 @@ __device__ __forceinline__ void conservative_dir(const KParams &p, const double 
                                                  double (&R)[5][4]) {
   using Gm = XYGeom<M>;
   constexpr int W = Gm::W;
+  constexpr bool PW = DIR == 0 && Gm::PAIRS;  // x-windows: 16-byte loads
   // hu = u_d / 2 (exact halving): every skew half and flux below uses it, so the
   // factors 1/2 cost nothing per term; (1/2 e + p) u_d = (e + 2p) hu exactly
   double hu[W], pw[W], v[W], t[W];
   double heat[4];
   {
     double r[W];
-    ldwin<W>(PR + XP_R * Gm::FSZ + base, st, r);
-    ldwin<W>(S + (XF_M0 + DIR) * Gm::FSZ + base, st, t);
+    ldwin<W, PW>(PR + XP_R * Gm::FSZ + base, st, r);
+    ldwin<W, PW>(S + (XF_M0 + DIR) * Gm::FSZ + base, st, t);
 #pragma unroll
     for (int k = 0; k < W; ++k) hu[k] = 0.5 * __dmul_rn(t[k], r[k]);
 #pragma unroll
     for (int j = 0; j < 4; ++j) R[0][j] = -0.5 * wd1<M, W>(p, t, j);
-    ldwin<W>(PR + XP_P * Gm::FSZ + base, st, pw);
+    ldwin<W, PW>(PR + XP_P * Gm::FSZ + base, st, pw);
     if (HEAT) {
 #pragma unroll
       for (int k = 0; k < W; ++k) v[k] = __dmul_rn(__dmul_rn(p.gM2, pw[k]), r[k]);
@@ -229,12 +251,12 @@ __device__ __forceinline__ void conservative_dir(const KParams &p, const double 
       for (int j = 0; j < 4; ++j) heat[j] = p.kappa * wd2<M, W>(p, v, j);
     }
   }
-  ldwin<W>(S + XF_RHO * Gm::FSZ + base, st, v);
+  ldwin<W, PW>(S + XF_RHO * Gm::FSZ + base, st, v);
 #pragma unroll
   for (int j = 0; j < 4; ++j) R[0][j] = fma(-hu[j + M], wd1<M, W>(p, v, j), R[0][j]);
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
-    ldwin<W>(S + (XF_M0 + i) * Gm::FSZ + base, st, v);
+    ldwin<W, PW>(S + (XF_M0 + i) * Gm::FSZ + base, st, v);
 #pragma unroll
     for (int k = 0; k < W; ++k)
       t[k] = (i == DIR) ? fma(v[k], hu[k], pw[k]) : __dmul_rn(v[k], hu[k]);
@@ -242,7 +264,7 @@ __device__ __forceinline__ void conservative_dir(const KParams &p, const double 
     for (int j = 0; j < 4; ++j)
       R[1 + i][j] = -fma(hu[j + M], wd1<M, W>(p, v, j), wd1<M, W>(p, t, j));
   }
-  ldwin<W>(S + XF_E * Gm::FSZ + base, st, v);
+  ldwin<W, PW>(S + XF_E * Gm::FSZ + base, st, v);
 #pragma unroll
   for (int k = 0; k < W; ++k) t[k] = __dmul_rn(fma(2.0, pw[k], v[k]), hu[k]);
 #pragma unroll
@@ -254,42 +276,79 @@ __device__ __forceinline__ void conservative_dir(const KParams &p, const double 
   }
 }
 
-// issue the asynchronous copies of plane z's operands into plane buffer PB
+// 16-byte asynchronous global -> shared copy (L2 only)
+__device__ __forceinline__ void cp_async16(double *smem, const double *gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+
+// Gather tables of a CTA (plane independent): cx[hx] = global x of halo column hx,
+// ry[hy] = (global y of halo row hy) * nx, through the periodic wrap or the mirror.
 template <int M, bool SYM>
+__device__ __forceinline__ void xy_tables(const KParams &p, int *cx, int *ry, int x0, int y0,
+                                          int tid, int nthr) {
+  using Gm = XYGeom<M>;
+  for (int i = tid; i < Gm::HX + Gm::HY; i += nthr) {
+    int f;
+    if (i < Gm::HX) cx[i] = bmap_t<SYM>(x0 - M + i, p.nx, p.sym[0], f);
+    else ry[i - Gm::HX] = bmap_t<SYM>(y0 - M + i - Gm::HX, p.ny, p.sym[1], f) * p.nx;
+  }
+}
+
+// issue the asynchronous copies of plane z's operands into plane buffer PB.
+// pairs: 16-byte copies of x-pairs (even m, even nx, periodic x: a pair never
+// straddles the wrap, since every halo row starts at an even x)
+template <int M>
 __device__ __forceinline__ void xy_issue_plane(const KParams &p, const double *__restrict__ q,
                                                const double *__restrict__ gz, double *PB, int z,
-                                               int x0, int y0, int tid, int nthr) {
+                                               const int *cx, const int *ry, int tid, int nthr,
+                                               bool pairs) {
   using Gm = XYGeom<M>;
-  constexpr int HX = Gm::HX, HY = Gm::HY, PX = Gm::PX, FSZ = Gm::FSZ;
+  constexpr int HX = Gm::HX, HY = Gm::HY, PX = Gm::PX, FSZ = Gm::FSZ, GP = Gm::GP;
   const size_t FS = (size_t)p.nx * p.ny;
   const double *qp = q + qplane(p, z);
   const double *gp = gz + (size_t)z * 3 * FS;
+  if (Gm::PAIRS && pairs) {
+    constexpr int H2 = HX / 2, T2 = XY_TX / 2;
 #pragma unroll 1
-  for (int idx = tid; idx < HY * HX; idx += nthr) {
-    const int hy = idx / HX, hx = idx - hy * HX;
-    int fx, fy;
-    const size_t off = (size_t)bmap_t<SYM>(y0 - M + hy, p.ny, p.sym[1], fy) * p.nx +
-                       bmap_t<SYM>(x0 - M + hx, p.nx, p.sym[0], fx);
-    double *d = PB + hy * PX + hx;
+    for (int idx = tid; idx < HY * H2; idx += nthr) {
+      const int hy = idx / H2, hx = 2 * (idx - hy * H2);
+      const int off = ry[hy] + cx[hx];
+      double *d = PB + hy * PX + hx;
 #pragma unroll
-    for (int f = 0; f < 5; ++f) cp_async8(d + f * FSZ, qp + f * FS + off);
-    cp_async8(d + XF_G22 * FSZ, gp + 2 * FS + off);
-  }
+      for (int f = 0; f < 5; ++f) cp_async16(d + f * FSZ, qp + f * FS + off);
+      cp_async16(d + XF_G22 * FSZ, gp + 2 * FS + off);
+    }
 #pragma unroll 1
-  for (int idx = tid; idx < XY_TY * HX; idx += nthr) {
-    const int ty = idx / HX, hx = idx - ty * HX;
-    int fx, fy;
-    const size_t off = (size_t)bmap_t<SYM>(y0 + ty, p.ny, p.sym[1], fy) * p.nx +
-                       bmap_t<SYM>(x0 - M + hx, p.nx, p.sym[0], fx);
-    cp_async8(PB + Gm::PB_G02 + ty * PX + hx, gp + off);
-  }
+    for (int idx = tid; idx < XY_TY * H2; idx += nthr) {
+      const int ty = idx / H2, hx = 2 * (idx - ty * H2);
+      cp_async16(PB + Gm::PB_G02 + ty * PX + hx, gp + ry[ty + M] + cx[hx]);
+    }
 #pragma unroll 1
-  for (int idx = tid; idx < HY * XY_TX; idx += nthr) {
-    const int hy = idx >> 5, tx = idx & 31;
-    int fx, fy;
-    const size_t off = (size_t)bmap_t<SYM>(y0 - M + hy, p.ny, p.sym[1], fy) * p.nx +
-                       bmap_t<SYM>(x0 + tx, p.nx, p.sym[0], fx);
-    cp_async8(PB + Gm::PB_G12 + hy * Gm::TP + tx, gp + FS + off);
+    for (int idx = tid; idx < HY * T2; idx += nthr) {
+      const int hy = idx / T2, tx = 2 * (idx - hy * T2);
+      cp_async16(PB + Gm::PB_G12 + hy * GP + tx, gp + FS + ry[hy] + cx[tx + M]);
+    }
+  } else {
+#pragma unroll 1
+    for (int idx = tid; idx < HY * HX; idx += nthr) {
+      const int hy = idx / HX, hx = idx - hy * HX;
+      const int off = ry[hy] + cx[hx];
+      double *d = PB + hy * PX + hx;
+#pragma unroll
+      for (int f = 0; f < 5; ++f) cp_async8(d + f * FSZ, qp + f * FS + off);
+      cp_async8(d + XF_G22 * FSZ, gp + 2 * FS + off);
+    }
+#pragma unroll 1
+    for (int idx = tid; idx < XY_TY * HX; idx += nthr) {
+      const int ty = idx / HX, hx = idx - ty * HX;
+      cp_async8(PB + Gm::PB_G02 + ty * PX + hx, gp + ry[ty + M] + cx[hx]);
+    }
+#pragma unroll 1
+    for (int idx = tid; idx < HY * XY_TX; idx += nthr) {
+      const int hy = idx >> 5, tx = idx & 31;
+      cp_async8(PB + Gm::PB_G12 + hy * GP + tx, gp + FS + ry[hy] + cx[tx + M]);
+    }
   }
   asm volatile("cp.async.commit_group;\n" ::: "memory");
 }
@@ -315,7 +374,7 @@ __device__ __forceinline__ void xy_mirror_signs(const KParams &p, double *PB, in
     if (fx) d[XF_M0 * FSZ] = -d[XF_M0 * FSZ];
     if (fy) d[XF_M1 * FSZ] = -d[XF_M1 * FSZ];
     if (fx && hy >= M && hy < M + XY_TY) PB[Gm::PB_G02 + (hy - M) * PX + hx] *= -1.0;
-    if (fy && hx >= M && hx < M + XY_TX) PB[Gm::PB_G12 + hy * Gm::TP + hx - M] *= -1.0;
+    if (fy && hx >= M && hx < M + XY_TX) PB[Gm::PB_G12 + hy * Gm::GP + hx - M] *= -1.0;
   }
 }
 
@@ -375,10 +434,14 @@ __global__ void __launch_bounds__(XY_CTA, 1)
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(XY_PROD_REGS) : "memory");
 #endif
     const int lane = tid - XY_THREADS;
+    int *cx = reinterpret_cast<int *>(SM + Gm::TOTAL), *ry = cx + Gm::HX;
+    xy_tables<M, SYM>(p, cx, ry, x0, y0, lane, XY_PROD);
+    nbar_sync(7, XY_PROD);  // tables complete (producers only)
+    const bool pairs = !SYM && (p.nx % 2) == 0;
     for (int i = 0; i < nplanes; ++i) {
       const int b = i & 1;
       if (i >= 2) nbar_sync(4 + b, XY_CTA);
-      xy_issue_plane<M, SYM>(p, q, gz, SM + b * Gm::PBSZ, zs + i, x0, y0, lane, XY_PROD);
+      xy_issue_plane<M>(p, q, gz, SM + b * Gm::PBSZ, zs + i, cx, ry, lane, XY_PROD, pairs);
       xy_prefetch_epilogue(p, TR ? qout + qplane(p, 0) : w, zs + i, x0, y0, lane, XY_PROD);
       if (TR && p.read_w) xy_prefetch_epilogue(p, w, zs + i, x0, y0, lane, XY_PROD);
       asm volatile("cp.async.wait_group 0;\n" ::: "memory");
@@ -478,10 +541,10 @@ __global__ void __launch_bounds__(XY_CTA, 1)
         const int base = hy * PX + seg * XY_RX;
         constexpr int W = Gm::W;
         double r[W], v[W], t[W];
-        ldwin<W>(PR + XP_R * FSZ + base, 1, r);
+        ldwin<W, Gm::PAIRS>(PR + XP_R * FSZ + base, 1, r);
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
-          ldwin<W>(S + (XF_M0 + i) * FSZ + base, 1, t);
+          ldwin<W, Gm::PAIRS>(S + (XF_M0 + i) * FSZ + base, 1, t);
 #pragma unroll
           for (int k = 0; k < W; ++k) v[k] = __dmul_rn(t[k], r[k]);
           double *Ei = i == 0 ? E0 : E1;
@@ -495,6 +558,7 @@ __global__ void __launch_bounds__(XY_CTA, 1)
         const int col = q7 & 31, seg = q7 >> 5;
         const int base = (seg * XY_RY) * PX + col + M;
         const int ebase = (seg * XY_RY) * TP + col;
+        const int gbase = (seg * XY_RY) * Gm::GP + col;
         double dTz[4];
         if (VAR) {  // D_z T of this thread's points (z-pass), loaded ahead of the stencils
 #pragma unroll
@@ -504,7 +568,7 @@ __global__ void __launch_bounds__(XY_CTA, 1)
           }
         }
         VelResult<M> o;
-        velocity_dir<M, 1, VAR>(p, S, PR, base, PX, G12 + ebase, TP, E0, E1, ebase, o);
+        velocity_dir<M, 1, VAR>(p, S, PR, base, PX, G12 + gbase, Gm::GP, E0, E1, ebase, o);
         if (VAR) {
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
@@ -514,7 +578,7 @@ __global__ void __launch_bounds__(XY_CTA, 1)
             const double g00 = E0[(ty + M) * TP + col], g10 = E1[(ty + M) * TP + col];
             const double g20 = XA[4 * NPT + pt];
             const double g01 = o.g[0][j], g11 = o.g[1][j], g21 = o.g[2][j];
-            const double g02 = G02[ty * PX + col + M], g12 = G12[(ty + M) * TP + col],
+            const double g02 = G02[ty * PX + col + M], g12 = G12[(ty + M) * Gm::GP + col],
                          g22 = S[XF_G22 * FSZ + c];
             const double T = o.Tc[j];
             const double mu = p.visc ? sutherland_mu(p, T) : 1.0;
@@ -570,7 +634,7 @@ __global__ void __launch_bounds__(XY_CTA, 1)
           const double g00 = E0[(ty + M) * TP + col], g10 = E1[(ty + M) * TP + col];
           const double g20 = XA[4 * NPT + pt];
           const double g01 = o.g[0][j], g11 = o.g[1][j], g21 = o.g[2][j];
-          const double g02 = G02[ty * PX + col + M], g12 = G12[(ty + M) * TP + col],
+          const double g02 = G02[ty * PX + col + M], g12 = G12[(ty + M) * Gm::GP + col],
                        g22 = S[XF_G22 * FSZ + c];
           // y-parts of V_i: V0 += nu (D11 u0 + 1/3 D1 g10);
           // V1 += nu (4/3 D11 u1 + 1/3 (D1 g00 + D1 g22)); V2 += nu (D11 u2 + 1/3 D1 g12)
