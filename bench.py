@@ -399,6 +399,15 @@ def main():
     torch.cuda.synchronize()
     diag_wall_ms = (time.perf_counter() - t_d) * 1e3 / n_diag
     diag_ms = d_ev0.elapsed_time(d_ev1) / n_diag
+    # the same diagnostics fused into every step (osbli_step_diag): K steps, each
+    # with the diagnostics of its input state, device-timed like the main region
+    torch.cuda.synchronize()
+    barrier()
+    d_ev0.record(stream)
+    solver.step_diag(args.steps)
+    d_ev1.record(stream)
+    torch.cuda.synchronize()
+    fused_ms_per_step = d_ev0.elapsed_time(d_ev1) / args.steps
 
     # ---- end to end through the public API with host buffers (pinned): every
     # step copies its input state in from the host and its result back out.
@@ -524,11 +533,16 @@ def main():
         "roofline": roof,
         "clocks": clocks,
         "gpu_launches": launches,
-        "diagnostics": {"ms_per_call": diag_ms, "wall_ms_per_call": diag_wall_ms,
+        "diagnostics": {"fused_ms_per_step": fused_ms_per_step,
+                        "fused_overhead_share": fused_ms_per_step / ms_per_step - 1.0,
+                        "ms_per_call": diag_ms, "wall_ms_per_call": diag_wall_ms,
                         "share_of_step": diag_ms / ms_per_step,
-                        "how": "osbli_diagnostics (E_k, enstrophy, dissipation) of the 256^3 "
-                               "state, CUDA events on the solver stream around 5 calls; "
-                               "wall_ms includes the host plane-order sum"},
+                        "how": "fused: osbli_step_diag(K) (diagnostics of every step's input "
+                               "state in its first xy-pass, host sums every 64 steps) timed "
+                               "like the main region; standalone: osbli_diagnostics (E_k, "
+                               "enstrophy, dissipation) of the state, CUDA events on the "
+                               "solver stream around 5 calls; wall_ms includes the host "
+                               "plane-order sum"},
         "e2e": {"value": e2e_value, "unit": "pt-steps/s", "h2d_bytes_per_step": state_bytes,
                 "d2h_bytes_per_step": state_bytes, "steps": args.e2e_steps,
                 "how": f"osbli_set_state_async (pinned host -> device), osbli_step(1), "

@@ -202,6 +202,19 @@ int osbli_get_state_async(osbli_ctx *h, double *q, int on_device); /* valid when
  * or NCCL failures. */
 int osbli_step(osbli_ctx *h, int n);
 
+/* Advance n >= 0 steps like osbli_step and return the diagnostics of the state
+ * at the start of every step: series[k] (k = 0..n-1) describes the state after
+ * step_count + k steps (t = that times dt), the same quantities as
+ * osbli_diagnostics, fused into each step's first xy-pass, which has
+ * every velocity gradient of that state in hand (per-(plane, tile) partials in a
+ * fixed order, planes summed in global z order: independent of the slab
+ * decomposition, within round-off of osbli_diagnostics, whose tiling differs).
+ * The state after the last step is not included (osbli_diagnostics gives it).
+ * Synchronises every 64 steps; collective when distributed (like
+ * osbli_diagnostics, including the non-finite check).  series must hold n
+ * entries.  INVAL on loopback slabs. */
+int osbli_step_diag(osbli_ctx *h, int n, osbli_diag *series);
+
 /* Diagnostics of the current state (collective over ranks when
  * distributed: every rank gets the same, decomposition-independent numbers, and
  * every rank returns OSBLI_E_NONFINITE if any rank's state went non-finite). */

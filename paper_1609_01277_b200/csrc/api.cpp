@@ -47,6 +47,10 @@ struct osbli_ctx {
   double *scratch = nullptr;  // diagnostics per-(plane, tile) partials
   double *nccl_part = nullptr;  // [nranks * max_nz][3] gathered plane partials
   unsigned int *flag_all = nullptr;  // max of the ranks' non-finite flags (device)
+  // fused diagnostics (osbli_step_diag): per-(plane, tile) partials of the stage-1
+  // xy-pass, per-step per-plane partials of a batch of steps, and their gather
+  double *dtiles = nullptr, *dseries = nullptr, *dseries_all = nullptr;
+  double *stage_dpart = nullptr;  // set while a stage 1 should write dtiles
   double *src = nullptr;        // optional source S, plane-major [nz][5][ny][nx]
   double *hflux_alloc = nullptr;  // H_j with ghost planes [nz + 2G][3][ny][nx] (cons form)
   int max_nz = 0;
@@ -132,6 +136,10 @@ void free_all(osbli_ctx *h) {
   cudaFree(h->nccl_part);
   cudaFree(h->flag_all);
   h->flag_all = nullptr;
+  cudaFree(h->dtiles);
+  cudaFree(h->dseries);
+  cudaFree(h->dseries_all);
+  h->dtiles = h->dseries = h->dseries_all = nullptr;
   cudaFree(h->src);
   h->src = nullptr;
   cudaFree(h->base.dtz);
@@ -522,6 +530,7 @@ int run_stage(osbli_ctx *h, int s, bool exchange = true, bool divh = true) {
   static const double RK2R_ALPHA[3] = {2.0 / 3.0, 5.0 / 12.0, 3.0 / 5.0};
   static const double RK2R_BETA[3] = {1.0 / 4.0, 3.0 / 20.0, 3.0 / 5.0};
   KParams p = h->base;
+  if (s == 0) p.dpart = h->stage_dpart;  // fused diagnostics of the step's input state
   double *qin = h->b.q[h->cur], *qout = h->b.q[h->cur ^ 1];
   double *wz = h->b.w;  // z-pass output W'
   if (h->scheme == OSBLI_RK3) {
@@ -689,6 +698,83 @@ int osbli_step(osbli_ctx *h, int n) {
       if (r) return r;
     }
     ++h->step_count;
+  }
+  return OSBLI_OK;
+}
+
+int osbli_step_diag(osbli_ctx *h, int n, osbli_diag *series) {
+  int u = check_usable(h);
+  if (u) return u;
+  if (n < 0 || (n > 0 && !series)) return fail(h, OSBLI_E_INVAL, "n must be >= 0 and series non-null");
+  if (h->loop) return fail(h, OSBLI_E_INVAL, "loopback slabs advance together: osbli_loopback_step");
+  constexpr int BATCH = 64;  // steps per gather / host reduction
+  const int ntiles = osbli::xypass_tiles(h->base);
+  const int stride = h->max_nz > h->nz ? h->max_nz : h->nz;  // planes per step record
+  const size_t rec = (size_t)3 * stride;                      // doubles per step record
+  if (!h->dtiles) {
+    CK(h, cudaStreamSynchronize(h->stream));
+    CK(h, cudaMalloc((void **)&h->dtiles, (size_t)3 * h->nz * ntiles * sizeof(double)));
+    CK(h, cudaMalloc((void **)&h->dseries, BATCH * rec * sizeof(double)));
+    CK(h, cudaMemset(h->dseries, 0, BATCH * rec * sizeof(double)));  // padding planes stay 0
+    if (h->comm)
+      CK(h, cudaMalloc((void **)&h->dseries_all, (size_t)h->nranks * BATCH * rec * sizeof(double)));
+  }
+  std::vector<double> host((size_t)(h->comm ? h->nranks : 1) * BATCH * rec);
+  std::vector<int> counts;
+  if (h->comm) {
+    for (int rr = 0; rr < h->nranks; ++rr) {
+      int z0 = 0, nzl = 0;
+      slab_partition(h->nz_global, h->nranks, rr, &z0, &nzl);
+      counts.push_back(nzl);
+    }
+  } else {
+    counts.push_back(h->nz);
+  }
+  const double N = (double)h->nx * h->ny * h->nz_global;
+  for (int k0 = 0; k0 < n; k0 += BATCH) {
+    const int nb = n - k0 < BATCH ? n - k0 : BATCH;
+    const long long step0 = h->step_count;
+    for (int b = 0; b < nb; ++b) {
+      for (int s = 0; s < nstages(h); ++s) {
+        h->stage_dpart = s == 0 ? h->dtiles : nullptr;
+        int r = run_stage(h, s);
+        h->stage_dpart = nullptr;
+        if (r) return r;
+        if (s == 0)
+          CK(h, osbli::launch_diag_planes(h->dtiles, h->nz, ntiles, h->dseries + b * rec,
+                                          h->stream, &h->launches));
+      }
+      ++h->step_count;
+    }
+    const double *src = h->dseries;
+    if (h->comm) {
+      NK(h, ncclAllGather(h->dseries, h->dseries_all, BATCH * rec, ncclDouble, h->comm, h->stream));
+      src = h->dseries_all;
+    }
+    CK(h, cudaMemcpyAsync(host.data(), src, host.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                          h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+    int r = check_flag(h);  // collective when distributed
+    if (r) return r;
+    for (int b = 0; b < nb; ++b) {
+      // Neumaier sums over planes in global z order (ranks own consecutive slabs)
+      double sm[3] = {0, 0, 0}, c[3] = {0, 0, 0};
+      for (int rr = 0; rr < (int)counts.size(); ++rr)
+        for (int z = 0; z < counts[rr]; ++z)
+          for (int k = 0; k < 3; ++k) {
+            const double x = host[((size_t)rr * BATCH + b) * rec + (size_t)3 * z + k];
+            const double t = sm[k] + x;
+            if (std::fabs(sm[k]) >= std::fabs(x)) c[k] += (sm[k] - t) + x;
+            else c[k] += (x - t) + sm[k];
+            sm[k] = t;
+          }
+      osbli_diag &d = series[k0 + b];
+      d.step = step0 + b;
+      d.t = d.step * h->dt;
+      d.kinetic_energy = (sm[0] + c[0]) / N;
+      d.enstrophy = (sm[1] + c[1]) / N;
+      d.dissipation = (sm[2] + c[2]) / N;
+    }
   }
   return OSBLI_OK;
 }

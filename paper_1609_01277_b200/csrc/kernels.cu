@@ -170,6 +170,15 @@ cudaError_t launch_stage(const KParams &p, const double *q_in, double *q_out, do
   return launch_divh(p, q_out, w, r_out, flag, 0, p.nz, s, launches);
 }
 
+int xypass_tiles(const KParams &p) { return ((p.nx + 31) / 32) * ((p.ny + 15) / 16); }
+
+cudaError_t launch_diag_planes(const double *tpart, int nz, int ntiles, double *part,
+                               cudaStream_t s, long long *launches) {
+  ++*launches;
+  diag_tiles_kernel<<<(3 * nz + 127) / 128, 128, 0, s>>>(tpart, nz, ntiles, part);
+  return cudaGetLastError();
+}
+
 size_t diagnostics_scratch(const KParams &p) {
   return (size_t)3 * p.nz * ((p.nx + 31) / 32) * ((p.ny + DG_TY - 1) / DG_TY);
 }

@@ -37,6 +37,9 @@ struct KParams {
   int cons;        // 1: viscous work in divergence form D_j H_j, H_j = u_i tau_ij
   double *dtz;     // variants: D_z T from the z-pass, [nz][ny][nx]
   double *hflux;   // cons: H_j from the xy-pass, [nz][3][ny][nx]
+  // fused diagnostics of the stage's input state (osbli_step_diag): the xy-pass
+  // writes per-(plane, tile) partials [nz][xy tiles][3] here when non-null
+  double *dpart;
 };
 
 // Device buffers of one handle.  Q buffers: [nz + 2G][5][ny][nx] (plane-major,
@@ -82,6 +85,13 @@ cudaError_t launch_xypass(const KParams &p, const double *q_in, double *q_out, d
                           const double *gz, double *r_out, unsigned int *flag, int z_begin,
                           int z_end, cudaStream_t s, long long *launches, int z_begin1 = 0,
                           int z_end1 = 0);
+
+// Number of xy-pass tiles of a plane (the fused diagnostics' partials per plane).
+int xypass_tiles(const KParams &p);
+// Per-plane partials [nz][3] = the (plane, tile) partials [nz][ntiles][3] summed in
+// tile order.
+cudaError_t launch_diag_planes(const double *tpart, int nz, int ntiles, double *part,
+                               cudaStream_t s, long long *launches);
 
 // Per-plane diagnostics partial sums [nz][3] (E_k, enstrophy, dissipation sums).
 // scratch: >= diagnostics_scratch(p) doubles (per-(plane, tile) partials).

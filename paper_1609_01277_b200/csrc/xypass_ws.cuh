@@ -86,7 +86,8 @@ struct XYGeom {
   static constexpr int OFF_XA = OFF_E1 + EXT;       // 5 x [TY][TP]
   static constexpr int OFF_XB = OFF_XA + 5 * NPT;   // 5 x [TY][TP]
   static constexpr int OFF_XT = OFF_XB + 5 * NPT;   // [TY][TP] D_x T (equation variants)
-  static constexpr int TOTAL = OFF_XT + NPT;
+  static constexpr int OFF_DG = OFF_XT + NPT;       // [4 warps][3] fused diagnostics partials
+  static constexpr int TOTAL = OFF_DG + 16;
   // producer gather tables (ints): global x of each halo column, y * nx of each halo row
   static constexpr int TAB_INTS = HX + HY;
   static constexpr int BYTES = TOTAL * (int)sizeof(double) + TAB_INTS * (int)sizeof(int);
@@ -392,6 +393,39 @@ __device__ __forceinline__ void xy_prefetch_epilogue(const KParams &p, const dou
   }
 }
 
+// Fused diagnostics (D-11, D-12) of the stage's input state, when the
+// stage carries p.dpart: the integrands 1/2 rho u.u, 1/2 rho |omega|^2 and
+// tau_ij du_i/dx_j of a point from the gradients group A has in hand
+__device__ __forceinline__ void diag_point(double rho, double u0, double u1, double u2,
+                                           double g01, double g02, double g10, double g12,
+                                           double g20, double g21, double phi, double (&dg)[3]) {
+  dg[0] += 0.5 * rho * (u0 * u0 + u1 * u1 + u2 * u2);
+  const double w0 = g21 - g12, w1 = g02 - g20, w2 = g10 - g01;
+  dg[1] += 0.5 * rho * (w0 * w0 + w1 * w1 + w2 * w2);
+  dg[2] += phi;
+}
+
+// group A's (plane, tile) partial sums in a fixed order (warp butterflies, then
+// the 4 warps in order) -> p.dpart[z][tile][3]; red: 12 doubles of shared memory
+__device__ __forceinline__ void diag_tile_sum(const KParams &p, double (&dg)[3], double *red,
+                                              int z, int q7) {
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dg[k] += __shfl_xor_sync(0xffffffffu, dg[k], o);
+  }
+  if ((q7 & 31) == 0) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) red[3 * (q7 >> 5) + k] = dg[k];
+  }
+  nbar_sync(1, 128);
+  if (q7 < 3) {
+    const double t = ((red[q7] + red[3 + q7]) + red[6 + q7]) + red[9 + q7];
+    const int tile = blockIdx.y * gridDim.x + blockIdx.x;
+    p.dpart[((size_t)z * gridDim.x * gridDim.y + tile) * 3 + q7] = t;
+  }
+}
+
 // Instantiations (XF bits), so that each feature costs the default path nothing:
 // SYM (2): symmetry boundaries in x or y (mirror maps and the sign fix-up).
 // TR (1): two-register RK3 epilogue (OSBLI_RK3_2R, kernels.h): W' is read from
@@ -569,6 +603,7 @@ __global__ void __launch_bounds__(XY_CTA, 1)
         }
         VelResult<M> o;
         velocity_dir<M, 1, VAR>(p, S, PR, base, PX, G12 + gbase, Gm::GP, E0, E1, ebase, o);
+        double dg[3] = {0.0, 0.0, 0.0};  // fused diagnostics sums of this thread's points
         if (VAR) {
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
@@ -603,6 +638,12 @@ __global__ void __launch_bounds__(XY_CTA, 1)
             const double heat =
                 p.kappa * fma(mu, o.d2T[j], dmu * (tx * tx + ty_ * ty_ + tz * tz));
             double e = XA[3 * NPT + pt] + heat;
+            if (p.dpart && x0 + col < p.nx && y0 + ty < p.ny) {
+              const double Phi = mu * (p.nu * (2.0 * (g00 * g00 + g11 * g11 + g22 * g22) +
+                                               s01 * s01 + s02 * s02 + s12 * s12 -
+                                               (2.0 / 3.0) * th * th));
+              diag_point(S[XF_RHO * FSZ + c], u0, u1, u2, g01, g02, g10, g12, g20, g21, Phi, dg);
+            }
             if (p.cons) {
               // H_j = u_i tau_ij for the divergence kernel (D-27)
               const double mn = mu * p.nu;
@@ -649,6 +690,8 @@ __global__ void __launch_bounds__(XY_CTA, 1)
           const double Phi = p.nu * (2.0 * (g00 * g00 + g11 * g11 + g22 * g22) + s01 * s01 +
                                      s02 * s02 + s12 * s12 - (2.0 / 3.0) * th * th);
           const double u0 = o.uc[0][j], u1 = o.uc[1][j], u2 = o.uc[2][j];
+          if (p.dpart && x0 + col < p.nx && y0 + ty < p.ny)
+            diag_point(S[XF_RHO * FSZ + c], u0, u1, u2, g01, g02, g10, g12, g20, g21, Phi, dg);
           const double ex = XA[3 * NPT + pt];  // u_i V_i^x (phase X; the heat flux is B's)
           // dilatation halves of the skew terms, -1/2 s (g00 + g11)
           XA[0 * NPT + pt] = -0.5 * S[XF_RHO * FSZ + c] * thxy;
@@ -658,6 +701,7 @@ __global__ void __launch_bounds__(XY_CTA, 1)
           XA[4 * NPT + pt] = fma(-0.5 * S[XF_E * FSZ + c], thxy,
                                  (ex + Phi) + (u0 * V0y + u1 * V1y + u2 * V2y));
         }
+        if (p.dpart) diag_tile_sum(p, dg, SM + Gm::OFF_DG, z, q7);
       }
       // A's part of every point of this tile is final: hand over to group B
       nbar_arrive(6, XY_THREADS);

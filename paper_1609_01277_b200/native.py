@@ -76,6 +76,7 @@ def load():
     L.osbli_get_state.argtypes = [H, vp, c_int]
     L.osbli_step.argtypes = [H, c_int]
     L.osbli_diagnostics.argtypes = [H, ctypes.POINTER(_Diag)]
+    L.osbli_step_diag.argtypes = [H, c_int, ctypes.POINTER(_Diag)]
     L.osbli_residual.argtypes = [H, vp, c_int]
     L.osbli_sync.argtypes = [H]
     L.osbli_set_kernel_timing.argtypes = [H, c_int]
@@ -246,6 +247,14 @@ class Solver:
         d = _Diag()
         self._check(self._L.osbli_diagnostics(self._h, ctypes.byref(d)))
         return Diagnostics(d.t, d.step, d.kinetic_energy, d.enstrophy, d.dissipation)
+
+    def step_diag(self, n: int = 1):
+        """Advance n steps; the diagnostics of each step's input state (fused into
+        the step's first xy-pass), as a list of n Diagnostics."""
+        arr = (_Diag * max(int(n), 1))()
+        self._check(self._L.osbli_step_diag(self._h, int(n), arr))
+        return [Diagnostics(d.t, d.step, d.kinetic_energy, d.enstrophy, d.dissipation)
+                for d in arr[:int(n)]]
 
     def sync(self):
         self._check(self._L.osbli_sync(self._h))

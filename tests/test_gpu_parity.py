@@ -368,3 +368,66 @@ def test_long_one_dimensional_grids(osbli, orc, shape, direction):
     s.step(2)
     Qo = orc.step(orc.OracleParams(*shape, order, dx, dt=dt, **phys), Q, 1, 2)
     assert np.all(relerr(s.get_state(), Qo) < TOL)
+
+
+# ---------------------------------------------------------------- fused diagnostics
+def test_tgv64_series_fused_vs_golden(osbli):
+    """BASELINE configs[1] through osbli_step_diag (diagnostics fused into every
+    step's first xy-pass): the E_k, enstrophy and dissipation series of the oracle
+    (tests/golden) to 1e-9 over the first 1000 steps."""
+    path = os.path.join(os.path.dirname(__file__), "golden", "tgv64_o4_rk3_series.csv")
+    gold = np.loadtxt(path, delimiter=",", comments="#", skiprows=2)
+    n, dt = 64, 3.385e-3
+    s = make(osbli, (n, n, n), 4, 2 * math.pi / n, dt)
+    s.set_state(tgv(n, n, n))
+    nsteps = int(gold[-1, 0]) + 1
+    series = s.step_diag(nsteps)
+    assert [d.step for d in series] == list(range(nsteps))
+    got = {d.step: np.array([d.kinetic_energy, d.enstrophy, d.dissipation]) for d in series}
+    worst = np.zeros(3)
+    for row in gold:
+        worst = np.maximum(worst, np.abs(got[int(row[0])] - row[2:5]) / np.abs(row[2:5]))
+    assert np.all(worst < 1e-9), worst
+
+
+@pytest.mark.parametrize("order,shape,variant", [(12, (40, 36, 33), ""), (8, (70, 33, 20), "v"),
+                                                 (4, (24, 20, 16), "c"), (6, (33, 17, 9), "s")])
+def test_fused_diagnostics_equal_standalone(osbli, orc, order, shape, variant):
+    """osbli_step_diag's series equals osbli_diagnostics of the same states (round-off:
+    the two sum the plane in different tilings) and the oracle's, with Sutherland
+    mu(T) (v), the conservative viscous work (c) and symmetry boundaries (s)."""
+    dx = 2 * math.pi / max(shape)
+    dt = 1e-3
+    Q = perturbed_tgv(*shape, dx=dx, amp=0.02)
+    a = make(osbli, shape, order, dx, dt)
+    b = make(osbli, shape, order, dx, dt)
+    op = orc.OracleParams(*shape, order, dx, dt=dt, **TGV_PHYS)
+    for s in (a, b):
+        if "v" in variant:
+            s.set_viscosity(osbli.OSBLI_VISC_SUTHERLAND, 110.4 / 288.0)
+        if "c" in variant:
+            s.set_energy_form(osbli.OSBLI_ENERGY_CONSERVATIVE)
+        if "s" in variant:
+            for d in range(3):
+                s.set_boundary(d, osbli.OSBLI_BC_SYMMETRY)
+        s.set_state(Q)
+    if "v" in variant:
+        op.visc_law, op.suth = 1, 110.4 / 288.0
+    if "c" in variant:
+        op.energy_form = 1
+    if "s" in variant:
+        op.sym = (1, 1, 1)
+    series = a.step_diag(3)
+    Qs = Q
+    for k in range(3):
+        d = b.diagnostics()
+        do = orc.diagnostics(op, Qs)
+        f = series[k]
+        assert f.step == k and d.step == k
+        for x, y, z in ((f.kinetic_energy, d.kinetic_energy, do[0]), (f.enstrophy, d.enstrophy, do[1]),
+                        (f.dissipation, d.dissipation, do[2])):
+            assert abs(x - y) <= 1e-13 * abs(y), (k, x, y)
+            assert abs(x - z) <= 1e-12 * abs(z), (k, x, z)
+        b.step(1)
+        Qs = orc.step(op, Qs, 1, 1)
+    assert np.array_equal(a.get_state(), b.get_state())

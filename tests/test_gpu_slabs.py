@@ -171,3 +171,22 @@ def test_loopback_member_destroyed_is_reported_not_crashed(osbli):
             grp.slabs[r].residual()
         assert ei.value.status == "E_STATE"
     grp.close()
+
+
+@pytest.mark.parametrize("schedule", [0, 2])
+def test_single_rank_nccl_fused_diagnostics_bitwise(osbli, schedule):
+    """osbli_step_diag through the distributed path (ncclAllGather of the per-step
+    plane partials, collective non-finite check) equals the single domain bitwise."""
+    shape, order = (24, 20, 26), 8
+    dx, dt = 2 * math.pi / 26, 1e-3
+    Q = perturbed_tgv(*shape, dx=dx, amp=0.05)
+    dist = osbli.Solver(*shape, order, dx, dt, rank=0, nranks=1, unique_id=osbli.nccl_unique_id(),
+                        **TGV_PHYS)
+    dist.set_slab_schedule(schedule)
+    ref = osbli.Solver(*shape, order, dx, dt, **TGV_PHYS)
+    out = []
+    for s in (dist, ref):
+        s.set_state(Q)
+        out.append([(d.kinetic_energy, d.enstrophy, d.dissipation) for d in s.step_diag(70)])
+    assert out[0] == out[1]
+    assert np.array_equal(dist.get_state(), ref.get_state())
