@@ -439,8 +439,10 @@ __global__ void __launch_bounds__(XY_CTA, 1)
                   double *__restrict__ rout,
                   unsigned int *__restrict__ flag, const PlaneRange zr) {
   // XF bits: 1 = two-register epilogue, 2 = symmetry in x/y, 4 = equation variants
-  // (mu(T), conservative viscous work), which take the other two at run time
+  // (mu(T), conservative viscous work), which take the other two at run time;
+  // 8 = fused diagnostics (stage 1 of osbli_step_diag)
   constexpr bool VAR = (XF & 4) != 0;
+  constexpr bool DIAG = (XF & 8) != 0;  // fused diagnostics into p.dpart (osbli_step_diag)
   constexpr bool SYM = VAR || (XF & 2) != 0;
   const bool TR = VAR ? p.two_reg != 0 : (XF & 1) != 0;
   double *XT = nullptr;
@@ -603,7 +605,7 @@ __global__ void __launch_bounds__(XY_CTA, 1)
         }
         VelResult<M> o;
         velocity_dir<M, 1, VAR>(p, S, PR, base, PX, G12 + gbase, Gm::GP, E0, E1, ebase, o);
-        double dg[3] = {0.0, 0.0, 0.0};  // fused diagnostics sums of this thread's points
+        double dg[3] = {0.0, 0.0, 0.0};  // fused diagnostics sums of this thread's points (DIAG)
         if (VAR) {
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
@@ -638,7 +640,7 @@ __global__ void __launch_bounds__(XY_CTA, 1)
             const double heat =
                 p.kappa * fma(mu, o.d2T[j], dmu * (tx * tx + ty_ * ty_ + tz * tz));
             double e = XA[3 * NPT + pt] + heat;
-            if (p.dpart && x0 + col < p.nx && y0 + ty < p.ny) {
+            if (DIAG && x0 + col < p.nx && y0 + ty < p.ny) {
               const double Phi = mu * (p.nu * (2.0 * (g00 * g00 + g11 * g11 + g22 * g22) +
                                                s01 * s01 + s02 * s02 + s12 * s12 -
                                                (2.0 / 3.0) * th * th));
@@ -690,7 +692,7 @@ __global__ void __launch_bounds__(XY_CTA, 1)
           const double Phi = p.nu * (2.0 * (g00 * g00 + g11 * g11 + g22 * g22) + s01 * s01 +
                                      s02 * s02 + s12 * s12 - (2.0 / 3.0) * th * th);
           const double u0 = o.uc[0][j], u1 = o.uc[1][j], u2 = o.uc[2][j];
-          if (p.dpart && x0 + col < p.nx && y0 + ty < p.ny)
+          if (DIAG && x0 + col < p.nx && y0 + ty < p.ny)
             diag_point(S[XF_RHO * FSZ + c], u0, u1, u2, g01, g02, g10, g12, g20, g21, Phi, dg);
           const double ex = XA[3 * NPT + pt];  // u_i V_i^x (phase X; the heat flux is B's)
           // dilatation halves of the skew terms, -1/2 s (g00 + g11)
@@ -701,7 +703,7 @@ __global__ void __launch_bounds__(XY_CTA, 1)
           XA[4 * NPT + pt] = fma(-0.5 * S[XF_E * FSZ + c], thxy,
                                  (ex + Phi) + (u0 * V0y + u1 * V1y + u2 * V2y));
         }
-        if (p.dpart) diag_tile_sum(p, dg, SM + Gm::OFF_DG, z, q7);
+        if (DIAG) diag_tile_sum(p, dg, SM + Gm::OFF_DG, z, q7);
       }
       // A's part of every point of this tile is final: hand over to group B
       nbar_arrive(6, XY_THREADS);
