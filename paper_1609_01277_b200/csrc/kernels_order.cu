@@ -28,6 +28,8 @@
 // This translation unit instantiates every order-dependent kernel for one
 // stencil half width M = OSBLI_M (the Makefile compiles it once per M, in
 // parallel); kernels.cu dispatches on the run-time order.
+#include <cstdlib>
+
 #include "device_common.cuh"
 #include "dispatch.h"
 
@@ -319,6 +321,18 @@ cudaError_t ensure_smem_attr(K kern, int smem, unsigned &done) {
   return e;
 }
 
+// OSBLI_NO_SPLIT=1 (testing): keep the production launch shape on small grids: no
+// z-segment split of the z-pass pencils, no halving of the xy-pass segments (so
+// that sanitizer runs on small grids reach the ring advance and the 8-plane
+// pipelines of the 256^3 configuration)
+inline bool no_split() {
+  static const int v = [] {
+    const char *e = std::getenv("OSBLI_NO_SPLIT");
+    return (e && e[0] == '1') ? 1 : 0;
+  }();
+  return v != 0;
+}
+
 template <int M>
 cudaError_t zpass_launch(const KParams &p, const double *q, double *w, double *gz, int zb, int ze,
                          int zb1, int ze1, cudaStream_t s) {
@@ -335,6 +349,7 @@ cudaError_t zpass_launch(const KParams &p, const double *q, double *w, double *g
   // split the z-range into segments only when the pencils alone do not fill ~2 waves
   int nseg = (2 * 148 + gx * gy - 1) / (gx * gy);
   nseg = nseg < 1 ? 1 : (nseg > chunks ? chunks : nseg);
+  if (no_split()) nseg = 1;
   int ntot = 0;
   const PlaneRange zr = plane_range(zb, ze, zb1, ze1, ((chunks + nseg - 1) / nseg) * ZP_TZ, &ntot);
   dim3 grid(gx * gy, 1, ntot);
@@ -366,7 +381,7 @@ cudaError_t xypass_launch(const KParams &p, const double *q, double *qout, doubl
   const int len = (ze - zb) > nz1 ? (ze - zb) : nz1;
   int seg = len < ws::XY_SEG ? len : ws::XY_SEG;
   auto ctas = [&](int sg) { return tiles * ((ze - zb + sg - 1) / sg + (nz1 + sg - 1) / sg); };
-  while (seg > 1 && ctas(seg) < 148) seg = (seg + 1) / 2;
+  while (!no_split() && seg > 1 && ctas(seg) < 148) seg = (seg + 1) / 2;
   int ntot = 0;
   const PlaneRange zr = plane_range(zb, ze, zb1, ze1, seg, &ntot);
   dim3 grid((p.nx + ws::XY_TX - 1) / ws::XY_TX, (p.ny + ws::XY_TY - 1) / ws::XY_TY, ntot);
