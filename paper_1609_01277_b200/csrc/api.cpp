@@ -207,6 +207,7 @@ int create_common(osbli_ctx *h) {
   p.gm1 = h->gamma - 1.0;
   p.gM2 = h->gamma * h->Minf * h->Minf;
   p.dt = h->dt;
+  p.dbg = h->b.flag;
   CK(h, cudaStreamSynchronize(h->stream));
   return OSBLI_OK;
 }

@@ -77,6 +77,29 @@ inline PlaneRange plane_range(int zb, int ze, int zb1, int ze1, int seg_len, int
   return r;
 }
 
+// Debug builds (tools/build_variant.sh dbg "-DOSBLI_DEBUG_CHECKS=1"): every staged
+// global load is bounds-checked against its buffer, and shared-memory buffers are
+// filled with NaN whenever they are handed back for reuse, so that a read racing a
+// hand-off, or of data never written, turns into a NaN the oracle comparison sees
+// (compute-sanitizer is not available on this pool).
+#ifndef OSBLI_DEBUG_CHECKS
+#define OSBLI_DEBUG_CHECKS 0
+#endif
+// index i of an access into a buffer of n doubles
+__device__ __forceinline__ bool dbg_in(const KParams &p, long long i, long long n) {
+#if OSBLI_DEBUG_CHECKS
+  if (i < 0 || i >= n) {
+    if (p.dbg) atomicOr(p.dbg, 2u);
+    return false;
+  }
+#endif
+  return true;
+}
+__device__ __forceinline__ long long qbuf_len(const KParams &p) {
+  return (long long)(p.nz + 2 * p.G) * 5 * p.nx * p.ny;
+}
+__device__ __forceinline__ double dbg_nan() { return __longlong_as_double(0x7ff8dead00000000ll); }
+
 __device__ __forceinline__ size_t qplane(const KParams &p, int z) {
   return (size_t)(z + p.G) * 5 * (size_t)p.nx * p.ny;
 }

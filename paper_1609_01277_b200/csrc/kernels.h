@@ -40,6 +40,10 @@ struct KParams {
   // fused diagnostics of the stage's input state (osbli_step_diag): the xy-pass
   // writes per-(plane, tile) partials [nz][xy tiles][3] here when non-null
   double *dpart;
+  // debug builds (-DOSBLI_DEBUG_CHECKS=1): bounds violations of the staged loads
+  // set bit 2 of this flag (the handle's non-finite flag: the next synchronising
+  // call then fails)
+  unsigned int *dbg;
 };
 
 // Device buffers of one handle.  Q buffers: [nz + 2G][5][ny][nx] (plane-major,

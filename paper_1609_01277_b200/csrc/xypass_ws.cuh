@@ -316,6 +316,10 @@ __device__ __forceinline__ void xy_issue_plane(const KParams &p, const double *_
       const int hy = idx / H2, hx = 2 * (idx - hy * H2);
       const int off = ry[hy] + cx[hx];
       double *d = PB + hy * PX + hx;
+      if (OSBLI_DEBUG_CHECKS && !(dbg_in(p, (qp - q) + 4 * FS + off + 1, qbuf_len(p)) &&
+                                  dbg_in(p, (qp - q) + off, qbuf_len(p)) &&
+                                  dbg_in(p, (gp - gz) + 2 * FS + off + 1, 3LL * p.nz * FS)))
+        continue;
 #pragma unroll
       for (int f = 0; f < 5; ++f) cp_async16(d + f * FSZ, qp + f * FS + off);
       cp_async16(d + XF_G22 * FSZ, gp + 2 * FS + off);
@@ -336,6 +340,10 @@ __device__ __forceinline__ void xy_issue_plane(const KParams &p, const double *_
       const int hy = idx / HX, hx = idx - hy * HX;
       const int off = ry[hy] + cx[hx];
       double *d = PB + hy * PX + hx;
+      if (OSBLI_DEBUG_CHECKS && !(dbg_in(p, (qp - q) + 4 * FS + off, qbuf_len(p)) &&
+                                  dbg_in(p, (qp - q) + off, qbuf_len(p)) &&
+                                  dbg_in(p, (gp - gz) + 2 * FS + off, 3LL * p.nz * FS)))
+        continue;
 #pragma unroll
       for (int f = 0; f < 5; ++f) cp_async8(d + f * FSZ, qp + f * FS + off);
       cp_async8(d + XF_G22 * FSZ, gp + 2 * FS + off);
@@ -477,6 +485,10 @@ __global__ void __launch_bounds__(XY_CTA, 1)
     for (int i = 0; i < nplanes; ++i) {
       const int b = i & 1;
       if (i >= 2) nbar_sync(4 + b, XY_CTA);
+      if (OSBLI_DEBUG_CHECKS) {  // a consumer still reading the released buffer reads NaN
+        for (int k = lane; k < Gm::PBSZ; k += XY_PROD) SM[b * Gm::PBSZ + k] = dbg_nan();
+        nbar_sync(7, XY_PROD);
+      }
       xy_issue_plane<M>(p, q, gz, SM + b * Gm::PBSZ, zs + i, cx, ry, lane, XY_PROD, pairs);
       xy_prefetch_epilogue(p, TR ? qout + qplane(p, 0) : w, zs + i, x0, y0, lane, XY_PROD);
       if (TR && p.read_w) xy_prefetch_epilogue(p, w, zs + i, x0, y0, lane, XY_PROD);
@@ -534,6 +546,10 @@ __global__ void __launch_bounds__(XY_CTA, 1)
         velocity_dir<M, 0, VAR>(p, S, PR, base, 1, G02 + row * PX + seg * XY_RX, 1, E0, E1, 0, o);
         // B has finished reading XA (its epilogue of the previous plane)
         if (i > 0) nbar_sync(10, XY_THREADS);
+        if (OSBLI_DEBUG_CHECKS) {
+          for (int k = q7; k < 5 * NPT; k += 128) XA[k] = dbg_nan();
+          nbar_sync(1, 128);
+        }
         if (VAR) {
           // variants: mu(T) scales the viscous parts (D-26); D_x T kept for phase Y;
           // the conservative form leaves u_i V_i to D_j H_j (D-27)
@@ -710,6 +726,10 @@ __global__ void __launch_bounds__(XY_CTA, 1)
       if (i + 2 < nplanes) nbar_arrive(4 + cur, XY_CTA);  // done with this plane buffer
       if (i + 1 < nplanes) {
         nbar_sync(9, XY_THREADS);                 // B has read PR of plane z
+        if (OSBLI_DEBUG_CHECKS) {
+          for (int k = q7; k < 2 * FSZ; k += 128) PR[k] = dbg_nan();
+          nbar_sync(1, 128);
+        }
         nbar_sync(2 + (cur ^ 1), XY_PROD + 128);  // plane z+1 landed
         formulas(SM + (cur ^ 1) * Gm::PBSZ);
       }

@@ -161,6 +161,9 @@ __global__ void __launch_bounds__(ZP_THREADS, OSBLI_ZP_MINB)
         const int pl = idx >> 5;
         int fl;
         const double *qp = q + qplane(p, zread_t<SYMZ>(p, zs - M + pl, fl)) + rowoff;
+        if (OSBLI_DEBUG_CHECKS && !(dbg_in(p, qp - q, qbuf_len(p)) &&
+                                    dbg_in(p, qp - q + 4 * FS, qbuf_len(p))))
+          qp = q;
 #pragma unroll
         for (int f = 0; f < 5; ++f) raw[it][f] = __ldg(qp + f * FS);
         if (fl) raw[it][3] = -raw[it][3];  // rho u_z is odd under a z mirror
@@ -180,6 +183,9 @@ __global__ void __launch_bounds__(ZP_THREADS, OSBLI_ZP_MINB)
       const int j = idx >> 5;
       int fl_;
       const double *qp = q + qplane(p, zread_t<SYMZ>(p, zs + kk * ZP_TZ + M + j, fl_)) + rowoff;
+      if (OSBLI_DEBUG_CHECKS && !(dbg_in(p, qp - q, qbuf_len(p)) &&
+                                  dbg_in(p, qp - q + 4 * FS, qbuf_len(p))))
+        qp = q;
 #pragma unroll
       for (int f = 0; f < 5; ++f) cp_async8(RB + (f * ZP_TZ + j) * 32 + lane, qp + f * FS);
     }
