@@ -50,6 +50,9 @@ __device__ __forceinline__ void nbar_sync(int id, int count) {
 __device__ __forceinline__ void nbar_arrive(int id, int count) {
   asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(count) : "memory");
 }
+#ifndef OSBLI_XY_SMSP_SPLIT
+#define OSBLI_XY_SMSP_SPLIT 0
+#endif
 #ifndef OSBLI_XY_SEG
 #define OSBLI_XY_SEG 8
 #endif
@@ -466,8 +469,16 @@ __global__ void __launch_bounds__(XY_CTA, 1)
   int zs, ze;
   if (!zr.segment(zs, ze)) return;
   const size_t FS = (size_t)p.nx * p.ny;
+#if OSBLI_XY_SMSP_SPLIT
+  // warps are spread over the 4 sub-partitions by warp id mod 4: group A on
+  // sub-partitions 0, 1 (warps 0, 1, 4, 5), group B on 2, 3 (warps 2, 3, 6, 7)
+  const int wid = tid >> 5;
+  const int grp = tid < XY_THREADS ? (wid >> 1) & 1 : 2;
+  const int q7 = (((wid >> 2) << 1) | (wid & 1)) * 32 + (tid & 31);
+#else
   const int grp = tid >> 7;  // 0: velocity group A, 1: conservative group B (warp-uniform)
   const int q7 = tid & 127;
+#endif
   bool bad = false;
 
   const int nplanes = ze - zs;
@@ -796,20 +807,25 @@ __global__ void __launch_bounds__(XY_CTA, 1)
             wn[f][j] = fma(p.dt, XA[f * NPT + pt] + (XB[f * NPT + pt] + R[f][j]), wp[f][j]);
         }
         const int mode = rout ? 0 : (TR ? 3 : (p.write_w ? 1 : 2));
+        // one uniform branch on the mode, the four points inside it (the executed
+        // code stays contiguous)
+        auto points = [&](auto &&store) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int ty = seg * XY_RY + j;
-          const int y = y0 + ty;
-          if (!xin || y >= p.ny) continue;
-          const int c = (ty + M) * PX + col + M;
-          const size_t o = (size_t)z * 5 * FS + (size_t)y * p.nx + x;
-          if (mode == 0) {
+          for (int j = 0; j < 4; ++j) {
+            const int ty = seg * XY_RY + j;
+            const int y = y0 + ty;
+            if (!xin || y >= p.ny) continue;
+            store(j, (ty + M) * PX + col + M, (size_t)z * 5 * FS + (size_t)y * p.nx + x,
+                  qout + qplane(p, z) + (size_t)y * p.nx + x);
+          }
+        };
+        if (mode == 0) {
+          points([&](int j, int, size_t o, double *) {
 #pragma unroll
             for (int f = 0; f < 5; ++f) rout[o + f * FS] = wn[f][j];
-            continue;
-          }
-          double *qo = qout + qplane(p, z) + (size_t)y * p.nx + x;
-          if (mode == 1) {  // 2N RK3 stages 1, 2: W <- W', Q' = Q + B W
+          });
+        } else if (mode == 1) {  // 2N RK3 stages 1, 2: W <- W', Q' = Q + B W
+          points([&](int j, int c, size_t o, double *qo) {
 #pragma unroll
             for (int f = 0; f < 5; ++f) {
               w[o + f * FS] = wn[f][j];
@@ -817,14 +833,18 @@ __global__ void __launch_bounds__(XY_CTA, 1)
               qo[f * FS] = qn;
               bad |= !isfinite(qn);
             }
-          } else if (mode == 2) {  // last stage / Euler: Q' = Q + B W
+          });
+        } else if (mode == 2) {  // last stage / Euler: Q' = Q + B W
+          points([&](int j, int c, size_t, double *qo) {
 #pragma unroll
             for (int f = 0; f < 5; ++f) {
               const double qn = fma(p.B, wn[f][j], S[fidx[f] * FSZ + c]);
               qo[f * FS] = qn;
               bad |= !isfinite(qn);
             }
-          } else {  // two-register RK3: w holds Q_old
+          });
+        } else {  // two-register RK3: w holds Q_old
+          points([&](int j, int c, size_t o, double *qo) {
 #pragma unroll
             for (int f = 0; f < 5; ++f) {
               const double qb = p.read_w ? qold[f][j] : S[fidx[f] * FSZ + c];
@@ -833,7 +853,7 @@ __global__ void __launch_bounds__(XY_CTA, 1)
               qo[f * FS] = qn;
               bad |= !isfinite(qn);
             }
-          }
+          });
         }
         if (i + 1 < nplanes) nbar_arrive(10, XY_THREADS);  // done with XA
         if (i + 2 < nplanes) nbar_arrive(4 + cur, XY_CTA);  // done with this plane buffer

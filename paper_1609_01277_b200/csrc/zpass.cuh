@@ -73,6 +73,12 @@ __device__ __forceinline__ void zstore(const KParams &p, double *S, int slot, in
   s[ZS_G * NR * 32] = (0.5 * e + pr) * u2;
 }
 
+// 16-byte asynchronous global -> shared copy (L2 only)
+__device__ __forceinline__ void cp_async16z(double *smem, const double *gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+
 // register window of ring field f starting at ring slot slot0 (wraps modulo NR)
 template <int M>
 __device__ __forceinline__ void zwindow(const double *S, int f, int slot0, int lane,
@@ -178,16 +184,34 @@ __global__ void __launch_bounds__(ZP_THREADS, OSBLI_ZP_MINB)
     }
   }
   // raw planes of chunk kk: z = zs + kk*TZ + M + j, j = 0..TZ-1  ->  RB[f][j][c]
+  // 16-byte copies of column pairs when the pencil lies inside the grid and rows
+  // start at even offsets (even nx: no pair straddles the periodic wrap)
+  const bool pairs = (p.nx % 2) == 0 && x0 + ZP_TX <= p.nx;
   auto issue_raw = [&](int kk) {
-    for (int idx = tid; idx < ZP_TZ * 32; idx += ZP_THREADS) {
-      const int j = idx >> 5;
-      int fl_;
-      const double *qp = q + qplane(p, zread_t<SYMZ>(p, zs + kk * ZP_TZ + M + j, fl_)) + rowoff;
-      if (OSBLI_DEBUG_CHECKS && !(dbg_in(p, qp - q, qbuf_len(p)) &&
-                                  dbg_in(p, qp - q + 4 * FS, qbuf_len(p))))
-        qp = q;
+    if (pairs) {
+      // lanes 0-15: plane j, columns 2l, 2l+1; lanes 16-31: plane j + 1
+      const int l2 = 2 * (lane & 15);
+      const size_t roff = (size_t)y * p.nx + x0 + l2;
+      for (int idx = 2 * warp + (lane >> 4); idx < ZP_TZ; idx += 2 * (ZP_THREADS / 32)) {
+        int fl_;
+        const double *qp = q + qplane(p, zread_t<SYMZ>(p, zs + kk * ZP_TZ + M + idx, fl_)) + roff;
+        if (OSBLI_DEBUG_CHECKS && !(dbg_in(p, qp - q, qbuf_len(p)) &&
+                                    dbg_in(p, qp - q + 4 * FS + 1, qbuf_len(p))))
+          qp = q;
 #pragma unroll
-      for (int f = 0; f < 5; ++f) cp_async8(RB + (f * ZP_TZ + j) * 32 + lane, qp + f * FS);
+        for (int f = 0; f < 5; ++f) cp_async16z(RB + (f * ZP_TZ + idx) * 32 + l2, qp + f * FS);
+      }
+    } else {
+      for (int idx = tid; idx < ZP_TZ * 32; idx += ZP_THREADS) {
+        const int j = idx >> 5;
+        int fl_;
+        const double *qp = q + qplane(p, zread_t<SYMZ>(p, zs + kk * ZP_TZ + M + j, fl_)) + rowoff;
+        if (OSBLI_DEBUG_CHECKS && !(dbg_in(p, qp - q, qbuf_len(p)) &&
+                                    dbg_in(p, qp - q + 4 * FS, qbuf_len(p))))
+          qp = q;
+#pragma unroll
+        for (int f = 0; f < 5; ++f) cp_async8(RB + (f * ZP_TZ + j) * 32 + lane, qp + f * FS);
+      }
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
