@@ -51,7 +51,7 @@ __device__ __forceinline__ void nbar_arrive(int id, int count) {
   asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(count) : "memory");
 }
 #ifndef OSBLI_XY_SMSP_SPLIT
-#define OSBLI_XY_SMSP_SPLIT 0
+#define OSBLI_XY_SMSP_SPLIT 1
 #endif
 #ifndef OSBLI_XY_SEG
 #define OSBLI_XY_SEG 8
