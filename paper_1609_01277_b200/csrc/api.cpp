@@ -19,6 +19,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "kernels.h"
 #include "weights.h"
 
@@ -74,6 +76,17 @@ struct osbli_ctx {
 };
 
 namespace {
+
+// NVTX ranges (SURVEY §5 tracing): every RK stage, its halo exchange, the
+// diagnostics reduction.  Header-only NVTX v3: a push/pop costs a few ns when no
+// tool is attached; under nsys/ncu the ranges put the host-side sequence
+// (exchange -> z-pass -> xy-pass) on the timeline next to the kernels.
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange &) = delete;
+  NvtxRange &operator=(const NvtxRange &) = delete;
+};
 
 thread_local std::string g_create_error;
 
@@ -263,6 +276,7 @@ template <typename Sibling>
 int exchange_planes(osbli_ctx *h, double *base, int nf, int odd, Sibling sibling,
                     cudaStream_t st) {
   if (!h->slab) return OSBLI_OK;
+  NvtxRange range(nf == 5 ? "osbli ghost exchange (Q)" : "osbli ghost exchange (H)");
   if (!st) st = h->stream;
   const int G = h->m;
   const size_t plane = (size_t)nf * h->nx * h->ny;
@@ -526,6 +540,8 @@ namespace {
 
 // One stage s of the time scheme on handle h: ghost exchange, z-pass, xy-pass.
 int run_stage(osbli_ctx *h, int s, bool exchange = true, bool divh = true) {
+  static const char *const kStageName[3] = {"osbli stage 1", "osbli stage 2", "osbli stage 3"};
+  NvtxRange range(kStageName[s]);
   static const double RK_A[3] = {0.0, -5.0 / 9.0, -153.0 / 128.0};
   static const double RK_B[3] = {1.0 / 3.0, 15.0 / 16.0, 8.0 / 15.0};
   static const double RK2R_ALPHA[3] = {2.0 / 3.0, 5.0 / 12.0, 3.0 / 5.0};
@@ -704,6 +720,7 @@ int osbli_step(osbli_ctx *h, int n) {
 }
 
 int osbli_step_diag(osbli_ctx *h, int n, osbli_diag *series) {
+  NvtxRange range("osbli step+diagnostics");
   int u = check_usable(h);
   if (u) return u;
   if (n < 0 || (n > 0 && !series)) return fail(h, OSBLI_E_INVAL, "n must be >= 0 and series non-null");
@@ -956,6 +973,7 @@ int osbli_set_source(osbli_ctx *h, const double *S, int on_device) {
 }
 
 int osbli_residual(osbli_ctx *h, double *R, int on_device) {
+  NvtxRange range("osbli residual");
   int u = check_usable(h);
   if (u) return u;
   if (!R) return fail(h, OSBLI_E_INVAL, "null output pointer");
@@ -985,6 +1003,7 @@ int osbli_residual(osbli_ctx *h, double *R, int on_device) {
 }
 
 int osbli_diagnostics(osbli_ctx *h, osbli_diag *out) {
+  NvtxRange range("osbli diagnostics");
   int u = check_usable(h);
   if (u) return u;
   if (!out) return fail(h, OSBLI_E_INVAL, "null output pointer");

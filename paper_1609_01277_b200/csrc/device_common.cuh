@@ -80,7 +80,7 @@ inline PlaneRange plane_range(int zb, int ze, int zb1, int ze1, int seg_len, int
 // Debug builds (tools/build_variant.sh dbg "-DOSBLI_DEBUG_CHECKS=1"): every staged
 // global load is bounds-checked against its buffer, and shared-memory buffers are
 // filled with NaN whenever they are handed back for reuse, so that a read racing a
-// hand-off, or of data never written, turns into a NaN the oracle comparison sees
+// hand-off, or of data never written, turns into a NaN the parity tests see
 // (compute-sanitizer is not available on this pool).
 #ifndef OSBLI_DEBUG_CHECKS
 #define OSBLI_DEBUG_CHECKS 0
