@@ -172,6 +172,9 @@ __device__ __forceinline__ double sutherland_dmu(const KParams &p, double T, dou
 
 // stencil sums: one dependent FMA chain per output (the four outputs of a register
 // window are independent); 2 interleaves two partial sums per output
+// #pragma unroll with a macro count (a count inside #pragma is not macro-expanded)
+#define OSBLI_PRAGMA(x) _Pragma(#x)
+#define OSBLI_UNROLL(n) OSBLI_PRAGMA(unroll n)
 #ifndef OSBLI_STENCIL_CHAINS
 #define OSBLI_STENCIL_CHAINS 1
 #endif

@@ -53,6 +53,17 @@ __device__ __forceinline__ void nbar_arrive(int id, int count) {
 #ifndef OSBLI_XY_SMSP_SPLIT
 #define OSBLI_XY_SMSP_SPLIT 1
 #endif
+#ifndef OSBLI_XY_FORM_UNROLL
+#define OSBLI_XY_FORM_UNROLL 1
+#endif
+// experiments only (results wrong): skip the plane staging after the first two
+// planes / skip the formulas after the first plane, to bound what each costs
+#ifndef OSBLI_XY_EXP_NOSTAGE
+#define OSBLI_XY_EXP_NOSTAGE 0
+#endif
+#ifndef OSBLI_XY_EXP_NOFORM
+#define OSBLI_XY_EXP_NOFORM 0
+#endif
 #ifndef OSBLI_XY_SEG
 #define OSBLI_XY_SEG 8
 #endif
@@ -500,7 +511,8 @@ __global__ void __launch_bounds__(XY_CTA, 1)
         for (int k = lane; k < Gm::PBSZ; k += XY_PROD) SM[b * Gm::PBSZ + k] = dbg_nan();
         nbar_sync(7, XY_PROD);
       }
-      xy_issue_plane<M>(p, q, gz, SM + b * Gm::PBSZ, zs + i, cx, ry, lane, XY_PROD, pairs);
+      if (!OSBLI_XY_EXP_NOSTAGE || i < 2)  // experiment: staging cost upper bound (wrong results)
+        xy_issue_plane<M>(p, q, gz, SM + b * Gm::PBSZ, zs + i, cx, ry, lane, XY_PROD, pairs);
       xy_prefetch_epilogue(p, TR ? qout + qplane(p, 0) : w, zs + i, x0, y0, lane, XY_PROD);
       if (TR && p.read_w) xy_prefetch_epilogue(p, w, zs + i, x0, y0, lane, XY_PROD);
       asm volatile("cp.async.wait_group 0;\n" ::: "memory");
@@ -528,7 +540,7 @@ __global__ void __launch_bounds__(XY_CTA, 1)
   if (grp == 0) {
     // formulas p and 1/rho once per point of a landed plane buffer
     auto formulas = [&](const double *Sb) {
-#pragma unroll 1
+OSBLI_UNROLL(OSBLI_XY_FORM_UNROLL)
       for (int idx = q7; idx < HY * HX; idx += 128) {
         const int hy = idx / HX, hx = idx - hy * HX;
         const int s = hy * PX + hx;
@@ -742,7 +754,7 @@ __global__ void __launch_bounds__(XY_CTA, 1)
           nbar_sync(1, 128);
         }
         nbar_sync(2 + (cur ^ 1), XY_PROD + 128);  // plane z+1 landed
-        formulas(SM + (cur ^ 1) * Gm::PBSZ);
+        if (!OSBLI_XY_EXP_NOFORM) formulas(SM + (cur ^ 1) * Gm::PBSZ);  // experiment flag: wrong results
       }
     }
   } else {

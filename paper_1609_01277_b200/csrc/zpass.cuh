@@ -23,6 +23,9 @@ constexpr int ZP_TX = 32;
 #ifndef OSBLI_ZP_RZ
 #define OSBLI_ZP_RZ 4
 #endif
+#ifndef OSBLI_ZP_ADV_UNROLL
+#define OSBLI_ZP_ADV_UNROLL 4
+#endif
 #ifndef OSBLI_ZP_MINB
 #define OSBLI_ZP_MINB 1
 #endif
@@ -341,6 +344,9 @@ __global__ void __launch_bounds__(ZP_THREADS, OSBLI_ZP_MINB)
       // ---- advance the ring: planes of chunk k+1 replace the first TZ planes of chunk k
       asm volatile("cp.async.wait_group 0;\n" ::: "memory");
       __syncthreads();  // staged raw planes visible; every warp is done with chunk k
+      // unrolled: the loads of all its points are in flight together (ZP_TZ*32 is a
+      // multiple of the block size)
+OSBLI_UNROLL(OSBLI_ZP_ADV_UNROLL)
       for (int idx = tid; idx < ZP_TZ * 32; idx += ZP_THREADS) {
         const int j = idx >> 5;
         const int slot = ((k + 1) * ZP_TZ + 2 * M + j) % NR;
