@@ -64,6 +64,19 @@ __device__ __forceinline__ void nbar_arrive(int id, int count) {
 #ifndef OSBLI_XY_EXP_NOFORM
 #define OSBLI_XY_EXP_NOFORM 0
 #endif
+// Work balance between the consumer groups (group A's chain p, 1/rho -> phase X
+// -> halo rows -> phase Y is the critical path): the x
+// mixed-derivative viscous parts nu/3 D_x g22, nu/3 D_x g02 are computed by group
+// B in its phase X (default; -1.1 % xy-pass at o12, -1.9 % at o8).  Moving the y
+// ones as well (MIXY_B) overshoots: B becomes the critical path (+2 %).
+#ifndef OSBLI_XY_MIXX_B
+#define OSBLI_XY_MIXX_B 1
+#endif
+constexpr bool XY_MIXX_B = OSBLI_XY_MIXX_B != 0;
+#ifndef OSBLI_XY_MIXY_B
+#define OSBLI_XY_MIXY_B 0
+#endif
+constexpr bool XY_MIXY_B = OSBLI_XY_MIXY_B != 0;
 #ifndef OSBLI_XY_SEG
 #define OSBLI_XY_SEG 8
 #endif
@@ -185,7 +198,7 @@ struct VelResult {
 
 // TW: also the temperature stencils (heat flux, and D_d T, T for the variants);
 // without them the heat flux is group B's (conservative_dir<.., HEAT = true>)
-template <int M, int DIR, bool TW>
+template <int M, int DIR, bool TW, bool NOMIX = false>
 __device__ __forceinline__ void velocity_dir(const KParams &p, const double *S, const double *PR,
                                              int base, int st, const double *gmix, int gst,
                                              const double *E0, const double *E1, int ebase,
@@ -218,12 +231,14 @@ __device__ __forceinline__ void velocity_dir(const KParams &p, const double *S, 
       o.Tc[j] = v[j + M];
     }
   }
-  ldwin<W, PW>(S + XF_G22 * Gm::FSZ + base, st, v);  // D_d g22
+  if (!NOMIX) {
+    ldwin<W, PW>(S + XF_G22 * Gm::FSZ + base, st, v);  // D_d g22
 #pragma unroll
-  for (int j = 0; j < 4; ++j) o.mixA[j] = wd1<M, W>(p, v, j);
-  ldwin<W, PW>(gmix, gst, v);  // DIR 0: D_x g02 = D_z g00 ; DIR 1: D_y g12 = D_z g11
+    for (int j = 0; j < 4; ++j) o.mixA[j] = wd1<M, W>(p, v, j);
+    ldwin<W, PW>(gmix, gst, v);  // DIR 0: D_x g02 = D_z g00 ; DIR 1: D_y g12 = D_z g11
 #pragma unroll
-  for (int j = 0; j < 4; ++j) o.mixB[j] = wd1<M, W>(p, v, j);
+    for (int j = 0; j < 4; ++j) o.mixB[j] = wd1<M, W>(p, v, j);
+  }
   if (DIR == 1) {
     ldwin<W>(E0 + ebase, Gm::TP, v);  // D_y g00
 #pragma unroll
@@ -256,8 +271,6 @@ __device__ __forceinline__ void conservative_dir(const KParams &p, const double 
     ldwin<W, PW>(S + (XF_M0 + DIR) * Gm::FSZ + base, st, t);
 #pragma unroll
     for (int k = 0; k < W; ++k) hu[k] = 0.5 * __dmul_rn(t[k], r[k]);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) R[0][j] = -0.5 * wd1<M, W>(p, t, j);
     ldwin<W, PW>(PR + XP_P * Gm::FSZ + base, st, pw);
     if (HEAT) {
 #pragma unroll
@@ -266,11 +279,30 @@ __device__ __forceinline__ void conservative_dir(const KParams &p, const double 
       for (int j = 0; j < 4; ++j) heat[j] = p.kappa * wd2<M, W>(p, v, j);
     }
   }
+  // D_d m_d serves the mass equation and the skew half of momentum d: one stencil
+  // of the m_d window for both (the variants' instantiation, HEAT = false, keeps
+  // the two separate: it is at its register limit)
+  if (!HEAT) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) R[0][j] = -0.5 * wd1<M, W>(p, t, j);
+  } else {
+    double dmd[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) dmd[j] = wd1<M, W>(p, t, j);
+#pragma unroll
+    for (int k = 0; k < W; ++k) v[k] = fma(t[k], hu[k], pw[k]);  // F_dd = 1/2 m_d u_d + p
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      R[0][j] = -0.5 * dmd[j];
+      R[1 + DIR][j] = -fma(hu[j + M], dmd[j], wd1<M, W>(p, v, j));
+    }
+  }
   ldwin<W, PW>(S + XF_RHO * Gm::FSZ + base, st, v);
 #pragma unroll
   for (int j = 0; j < 4; ++j) R[0][j] = fma(-hu[j + M], wd1<M, W>(p, v, j), R[0][j]);
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
+    if (HEAT && i == DIR) continue;
     ldwin<W, PW>(S + (XF_M0 + i) * Gm::FSZ + base, st, v);
 #pragma unroll
     for (int k = 0; k < W; ++k)
@@ -467,6 +499,10 @@ __global__ void __launch_bounds__(XY_CTA, 1)
   constexpr bool DIAG = (XF & 8) != 0;  // fused diagnostics into p.dpart (osbli_step_diag)
   constexpr bool SYM = VAR || (XF & 2) != 0;
   const bool TR = VAR ? p.two_reg != 0 : (XF & 1) != 0;
+  // group B takes the x mixed-derivative parts (XY_MIXX_B) in the default and
+  // diagnostics instantiations; the two-register epilogue holds Q_old in B's
+  // registers, and there the move would spill
+  constexpr bool MIXB = !VAR && XY_MIXX_B && (XF & 1) == 0;
   double *XT = nullptr;
   using Gm = XYGeom<M>;
   constexpr int HX = Gm::HX, HY = Gm::HY, PX = Gm::PX, FSZ = Gm::FSZ, NPT = Gm::NPT, TP = Gm::TP;
@@ -566,7 +602,8 @@ OSBLI_UNROLL(OSBLI_XY_FORM_UNROLL)
         const int base = hy * PX + seg * XY_RX;  // window start (halo coords)
         const int pt0 = row * TP + seg * XY_RX;
         VelResult<M> o;
-        velocity_dir<M, 0, VAR>(p, S, PR, base, 1, G02 + row * PX + seg * XY_RX, 1, E0, E1, 0, o);
+        velocity_dir<M, 0, VAR, MIXB>(
+            p, S, PR, base, 1, G02 + row * PX + seg * XY_RX, 1, E0, E1, 0, o);
         // B has finished reading XA (its epilogue of the previous plane)
         if (i > 0) nbar_sync(10, XY_THREADS);
         if (OSBLI_DEBUG_CHECKS) {
@@ -597,13 +634,15 @@ OSBLI_UNROLL(OSBLI_XY_FORM_UNROLL)
         for (int j = 0; j < 4; ++j) {
           // x-parts of V_i: V0 += nu (4/3 D00 u0 + 1/3 D0 g22); V1 += nu D00 u1;
           // V2 += nu (D00 u2 + 1/3 D0 g02)
-          const double V0 = p.nu * (o.d2u[0][j] + third * (o.d2u[0][j] + o.mixA[j]));
+          // (MIXB: the 1/3 D0 g22 and 1/3 D0 g02 parts are group B's)
+          const double V0 = p.nu * (o.d2u[0][j] + third * (o.d2u[0][j] + (MIXB ? 0.0 : o.mixA[j])));
           const double V1 = p.nu * o.d2u[1][j];
-          const double V2 = p.nu * (o.d2u[2][j] + third * o.mixB[j]);
+          const double V2 = p.nu * (o.d2u[2][j] + (MIXB ? 0.0 : third * o.mixB[j]));
           XA[0 * NPT + pt0 + j] = V0;
           XA[1 * NPT + pt0 + j] = V1;
           XA[2 * NPT + pt0 + j] = V2;
-          XA[3 * NPT + pt0 + j] = o.uc[0][j] * V0 + o.uc[1][j] * V1 + o.uc[2][j] * V2;
+          const double uv = o.uc[0][j] * V0 + o.uc[1][j] * V1 + o.uc[2][j] * V2;
+          XA[3 * NPT + pt0 + j] = uv;
           XA[4 * NPT + pt0 + j] = o.g[2][j];          // g20
           E0[hy * TP + seg * XY_RX + j] = o.g[0][j];  // g00
           E1[hy * TP + seg * XY_RX + j] = o.g[1][j];  // g10
@@ -643,7 +682,8 @@ OSBLI_UNROLL(OSBLI_XY_FORM_UNROLL)
           }
         }
         VelResult<M> o;
-        velocity_dir<M, 1, VAR>(p, S, PR, base, PX, G12 + gbase, Gm::GP, E0, E1, ebase, o);
+        velocity_dir<M, 1, VAR, !VAR && XY_MIXY_B>(p, S, PR, base, PX, G12 + gbase, Gm::GP, E0,
+                                                          E1, ebase, o);
         double dg[3] = {0.0, 0.0, 0.0};  // fused diagnostics sums of this thread's points (DIAG)
         if (VAR) {
 #pragma unroll
@@ -721,8 +761,10 @@ OSBLI_UNROLL(OSBLI_XY_FORM_UNROLL)
           // y-parts of V_i: V0 += nu (D11 u0 + 1/3 D1 g10);
           // V1 += nu (4/3 D11 u1 + 1/3 (D1 g00 + D1 g22)); V2 += nu (D11 u2 + 1/3 D1 g12)
           const double V0y = p.nu * (o.d2u[0][j] + third * o.mixD[j]);
-          const double V1y = p.nu * (o.d2u[1][j] + third * (o.d2u[1][j] + o.mixC[j] + o.mixA[j]));
-          const double V2y = p.nu * (o.d2u[2][j] + third * o.mixB[j]);
+          // (XY_MIXY_B: the 1/3 D1 g22 and 1/3 D1 g12 parts are group B's)
+          const double V1y = p.nu * (o.d2u[1][j] + third * (o.d2u[1][j] + o.mixC[j] +
+                                                            (XY_MIXY_B ? 0.0 : o.mixA[j])));
+          const double V2y = p.nu * (o.d2u[2][j] + (XY_MIXY_B ? 0.0 : third * o.mixB[j]));
           const double V0 = XA[0 * NPT + pt] + V0y, V1 = XA[1 * NPT + pt] + V1y,
                        V2 = XA[2 * NPT + pt] + V2y;
           const double thxy = g00 + g11, th = thxy + g22;
@@ -769,6 +811,26 @@ OSBLI_UNROLL(OSBLI_XY_FORM_UNROLL)
         const int pt0 = row * TP + seg * XY_RX;
         double R[5][4];
         conservative_dir<M, 0, !VAR>(p, S, PR, base, 1, R);
+        if (MIXB) {
+          // the x mixed-derivative viscous parts, nu/3 D_x g22 (momentum x) and
+          // nu/3 D_x g02 (momentum z), and their work u_i V_i (D-7)
+          constexpr int W = Gm::W;
+          double v[W], ma[4];
+          ldwin<W, Gm::PAIRS>(S + XF_G22 * FSZ + base, 1, v);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) ma[j] = (p.nu * third) * wd1<M, W>(p, v, j);
+          ldwin<W, Gm::PAIRS>(S + Gm::PB_G02 + row * PX + seg * XY_RX, 1, v);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const double mb = (p.nu * third) * wd1<M, W>(p, v, j);
+            const int c = base + M + j;
+            const double r = PR[XP_R * FSZ + c];
+            const double u0 = __dmul_rn(S[XF_M0 * FSZ + c], r), u2 = __dmul_rn(S[XF_M2 * FSZ + c], r);
+            R[1][j] += ma[j];
+            R[3][j] += mb;
+            R[4][j] = fma(u0, ma[j], fma(u2, mb, R[4][j]));
+          }
+        }
 #pragma unroll
         for (int f = 0; f < 5; ++f)
 #pragma unroll
@@ -792,6 +854,26 @@ OSBLI_UNROLL(OSBLI_XY_FORM_UNROLL)
         }
         double R[5][4];
         conservative_dir<M, 1, !VAR>(p, S, PR, base, PX, R);
+        if (!VAR && XY_MIXY_B) {
+          // the y mixed-derivative viscous parts, nu/3 D_y g22 (momentum y) and
+          // nu/3 D_y g12 (momentum z), and their work u_i V_i (D-7)
+          constexpr int W = Gm::W;
+          double v[W], ma[4];
+          ldwin<W>(S + XF_G22 * FSZ + base, PX, v);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) ma[j] = (p.nu * third) * wd1<M, W>(p, v, j);
+          ldwin<W>(S + Gm::PB_G12 + (seg * XY_RY) * Gm::GP + col, Gm::GP, v);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const double mb = (p.nu * third) * wd1<M, W>(p, v, j);
+            const int c = base + (M + j) * PX;
+            const double r = PR[XP_R * FSZ + c];
+            const double u1 = __dmul_rn(S[XF_M1 * FSZ + c], r), u2 = __dmul_rn(S[XF_M2 * FSZ + c], r);
+            R[2][j] += ma[j];
+            R[3][j] += mb;
+            R[4][j] = fma(u1, ma[j], fma(u2, mb, R[4][j]));
+          }
+        }
         if (i + 1 < nplanes) nbar_arrive(9, XY_THREADS);  // done with PR: A may refill it
         // two-register RK3: the register Q_old of the four points, loaded before
         // the hand-over wait so that its latency hides behind it
