@@ -353,6 +353,12 @@ cudaError_t zpass_launch(const KParams &p, const double *q, double *w, double *g
   int ntot = 0;
   const PlaneRange zr = plane_range(zb, ze, zb1, ze1, ((chunks + nseg - 1) / nseg) * ZP_TZ, &ntot);
   dim3 grid(gx * gy, 1, ntot);
+#if OSBLI_ZP_PERSIST
+  {  // experiment: OSBLI_ZP_GRID persistent CTAs per z segment
+    static const int g = [] { const char *e = std::getenv("OSBLI_ZP_GRID"); return e ? std::atoi(e) : 0; }();
+    if (g > 0 && g < gx * gy) grid.x = g;
+  }
+#endif
   kern<<<grid, ZP_THREADS, smem, s>>>(p, q, w, gz, zr);
   return cudaGetLastError();
 }
@@ -375,11 +381,11 @@ cudaError_t xypass_launch(const KParams &p, const double *q, double *qout, doubl
   static unsigned done[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   cudaError_t e = ensure_smem_attr(kern, smem, done[v]);
   if (e != cudaSuccess) return e;
-  // planes per CTA: XY_SEG, halved while the grid would not cover the SMs (small grids)
+  // planes per CTA: xy_seg<M>, halved while the grid would not cover the SMs (small grids)
   const int tiles = ((p.nx + ws::XY_TX - 1) / ws::XY_TX) * ((p.ny + ws::XY_TY - 1) / ws::XY_TY);
   const int nz1 = ze1 > zb1 ? ze1 - zb1 : 0;
   const int len = (ze - zb) > nz1 ? (ze - zb) : nz1;
-  int seg = len < ws::XY_SEG ? len : ws::XY_SEG;
+  int seg = len < ws::xy_seg<M>() ? len : ws::xy_seg<M>();
   auto ctas = [&](int sg) { return tiles * ((ze - zb + sg - 1) / sg + (nz1 + sg - 1) / sg); };
   while (!no_split() && seg > 1 && ctas(seg) < 148) seg = (seg + 1) / 2;
   int ntot = 0;

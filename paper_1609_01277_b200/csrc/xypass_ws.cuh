@@ -77,24 +77,35 @@ constexpr bool XY_MIXX_B = OSBLI_XY_MIXX_B != 0;
 #define OSBLI_XY_MIXY_B 0
 #endif
 constexpr bool XY_MIXY_B = OSBLI_XY_MIXY_B != 0;
+// z-planes per CTA: 16 at orders 2 and 4 (the pipeline fill of a segment weighs
+// more against the short stencils: -3 % xy-pass at o4), 8 above (neutral at 16)
 #ifndef OSBLI_XY_SEG
-#define OSBLI_XY_SEG 8
+template <int M>
+constexpr int xy_seg() { return M <= 2 ? 16 : 8; }
+#else
+template <int M>
+constexpr int xy_seg() { return OSBLI_XY_SEG; }
 #endif
-constexpr int XY_SEG = OSBLI_XY_SEG;  // z-planes per CTA
 // full-halo fields of a plane buffer (S) and of the per-plane formula arrays (PR)
 enum { XF_RHO = 0, XF_M0, XF_M1, XF_M2, XF_E, XF_G22, XF_N };
 enum { XP_P = 0, XP_R = 1 };
 
 template <int M>
 struct XYGeom {
-  static constexpr int HX = XY_TX + 2 * M;
-  // Even m (orders 4, 8, 12): the halo row starts at an even x, so it is copied in
-  // 16-byte pairs and the x-windows are read with 16-byte loads; a pitch of 2 mod 4
-  // doubles keeps those loads conflict-free for the row-per-lane access of phase X
-  // (8 lanes of a quarter warp on 8 rows hit 8 distinct 16-byte bank groups).
-  // Odd m: an odd pitch keeps the 8-byte row-per-lane loads conflict-free.
-  static constexpr bool PAIRS = (M % 2) == 0;
-  static constexpr int PX = PAIRS ? ((HX % 4 == 0) ? HX + 2 : HX) : (HX | 1);
+  // Staged columns start at the even x0 - M - XO: for odd m one extra column on
+  // each side (XO = 1), so that every halo row is copied in 16-byte pairs and the
+  // x-windows are read with 16-byte loads at every order (an odd-m window starts
+  // one double past a pair boundary: m + 3 pairs, the outer two values unused).
+  // A pitch of 2 mod 4 doubles keeps those loads conflict-free for the
+  // row-per-lane access of phase X (8 lanes of a quarter warp on 8 rows hit 8
+  // distinct 16-byte bank groups).  XC = staged column of the tile's x = 0.
+  static constexpr int XO = M % 2;
+  static constexpr int XC = M + XO;
+  static constexpr int HX = XY_TX + 2 * XC;  // staged columns (even)
+  static constexpr bool PAIRS = true;
+  // x-window load mode (ldwin): 1 = pairs from an aligned start, 2 = pairs from one before
+  static constexpr int XW = XO ? 2 : 1;
+  static constexpr int PX = (HX % 4 == 0) ? HX + 2 : HX;
   static constexpr int HY = XY_TY + 2 * M;
   static constexpr int FSZ = HY * PX;       // one full-halo field
   static constexpr int TP = XY_TX + 1;      // odd row pitch of tile-column arrays
@@ -129,17 +140,26 @@ constexpr int xy_smem_bytes() {
 // compiler may otherwise contract a product into the stencil difference
 // (f+ - f-) differently for different taps, and a uniform state would no
 // longer cancel exactly (SURVEY §8(c) equilibrium pin).
-// window of W values starting at base, stride `st` (doubles); PAIR: consecutive
-// values (st = 1) from a 16-byte aligned base, read as W/2 16-byte loads
-template <int W, bool PAIR = false>
+// window of W values starting at base, stride `st` (doubles).  PAIR = 1:
+// consecutive values (st = 1) from a 16-byte aligned base, read as W/2 16-byte
+// loads; PAIR = 2: base is one double past a 16-byte boundary, read as W/2 + 1
+// 16-byte loads from base - 1 (first and last values unused)
+template <int W, int PAIR = 0>
 __device__ __forceinline__ void ldwin(const double *base, int st, double (&v)[W]) {
-  if (PAIR) {
-    static_assert(W % 2 == 0, "pair windows need an even length");
+  static_assert(PAIR == 0 || W % 2 == 0, "pair windows need an even length");
+  if (PAIR == 1) {
 #pragma unroll
     for (int k = 0; k < W / 2; ++k) {
       const double2 t = reinterpret_cast<const double2 *>(base)[k];
       v[2 * k] = t.x;
       v[2 * k + 1] = t.y;
+    }
+  } else if (PAIR == 2) {
+#pragma unroll
+    for (int k = 0; k <= W / 2; ++k) {
+      const double2 t = reinterpret_cast<const double2 *>(base - 1)[k];
+      if (k > 0) v[2 * k - 1] = t.x;
+      if (k < W / 2) v[2 * k] = t.y;
     }
   } else {
 #pragma unroll
@@ -205,7 +225,7 @@ __device__ __forceinline__ void velocity_dir(const KParams &p, const double *S, 
                                              VelResult<M> &o) {
   using Gm = XYGeom<M>;
   constexpr int W = Gm::W;
-  constexpr bool PW = DIR == 0 && Gm::PAIRS;  // x-windows: 16-byte loads
+  constexpr int PW = DIR == 0 ? Gm::XW : 0;  // x-windows: 16-byte loads
   double r[W], v[W], t[W];
   ldwin<W, PW>(PR + XP_R * Gm::FSZ + base, st, r);
 #pragma unroll
@@ -260,7 +280,7 @@ __device__ __forceinline__ void conservative_dir(const KParams &p, const double 
                                                  double (&R)[5][4]) {
   using Gm = XYGeom<M>;
   constexpr int W = Gm::W;
-  constexpr bool PW = DIR == 0 && Gm::PAIRS;  // x-windows: 16-byte loads
+  constexpr int PW = DIR == 0 ? Gm::XW : 0;  // x-windows: 16-byte loads
   // hu = u_d / 2 (exact halving): every skew half and flux below uses it, so the
   // factors 1/2 cost nothing per term; (1/2 e + p) u_d = (e + 2p) hu exactly
   double hu[W], pw[W], v[W], t[W];
@@ -337,7 +357,7 @@ __device__ __forceinline__ void xy_tables(const KParams &p, int *cx, int *ry, in
   using Gm = XYGeom<M>;
   for (int i = tid; i < Gm::HX + Gm::HY; i += nthr) {
     int f;
-    if (i < Gm::HX) cx[i] = bmap_t<SYM>(x0 - M + i, p.nx, p.sym[0], f);
+    if (i < Gm::HX) cx[i] = bmap_t<SYM>(x0 - Gm::XC + i, p.nx, p.sym[0], f);
     else ry[i - Gm::HX] = bmap_t<SYM>(y0 - M + i - Gm::HX, p.ny, p.sym[1], f) * p.nx;
   }
 }
@@ -378,7 +398,7 @@ __device__ __forceinline__ void xy_issue_plane(const KParams &p, const double *_
 #pragma unroll 1
     for (int idx = tid; idx < HY * T2; idx += nthr) {
       const int hy = idx / T2, tx = 2 * (idx - hy * T2);
-      cp_async16(PB + Gm::PB_G12 + hy * GP + tx, gp + FS + ry[hy] + cx[tx + M]);
+      cp_async16(PB + Gm::PB_G12 + hy * GP + tx, gp + FS + ry[hy] + cx[tx + Gm::XC]);
     }
   } else {
 #pragma unroll 1
@@ -402,7 +422,7 @@ __device__ __forceinline__ void xy_issue_plane(const KParams &p, const double *_
 #pragma unroll 1
     for (int idx = tid; idx < HY * XY_TX; idx += nthr) {
       const int hy = idx >> 5, tx = idx & 31;
-      cp_async8(PB + Gm::PB_G12 + hy * GP + tx, gp + FS + ry[hy] + cx[tx + M]);
+      cp_async8(PB + Gm::PB_G12 + hy * GP + tx, gp + FS + ry[hy] + cx[tx + Gm::XC]);
     }
   }
   asm volatile("cp.async.commit_group;\n" ::: "memory");
@@ -416,20 +436,20 @@ __device__ __forceinline__ void xy_mirror_signs(const KParams &p, double *PB, in
                                                 int tid, int nthr) {
   using Gm = XYGeom<M>;
   constexpr int HX = Gm::HX, HY = Gm::HY, PX = Gm::PX, FSZ = Gm::FSZ;
-  const bool xs = p.sym[0] && (x0 - M < 0 || x0 + XY_TX + M > p.nx);
+  const bool xs = p.sym[0] && (x0 - Gm::XC < 0 || x0 + XY_TX + Gm::XC > p.nx);
   const bool ys = p.sym[1] && (y0 - M < 0 || y0 + XY_TY + M > p.ny);
   if (!xs && !ys) return;
 #pragma unroll 1
   for (int idx = tid; idx < HY * HX; idx += nthr) {
     const int hy = idx / HX, hx = idx - hy * HX;
     int fx, fy;
-    bmap(x0 - M + hx, p.nx, p.sym[0], fx);
+    bmap(x0 - Gm::XC + hx, p.nx, p.sym[0], fx);
     bmap(y0 - M + hy, p.ny, p.sym[1], fy);
     double *d = PB + hy * PX + hx;
     if (fx) d[XF_M0 * FSZ] = -d[XF_M0 * FSZ];
     if (fy) d[XF_M1 * FSZ] = -d[XF_M1 * FSZ];
     if (fx && hy >= M && hy < M + XY_TY) PB[Gm::PB_G02 + (hy - M) * PX + hx] *= -1.0;
-    if (fy && hx >= M && hx < M + XY_TX) PB[Gm::PB_G12 + hy * Gm::GP + hx - M] *= -1.0;
+    if (fy && hx >= Gm::XC && hx < Gm::XC + XY_TX) PB[Gm::PB_G12 + hy * Gm::GP + hx - Gm::XC] *= -1.0;
   }
 }
 
@@ -506,6 +526,7 @@ __global__ void __launch_bounds__(XY_CTA, 1)
   double *XT = nullptr;
   using Gm = XYGeom<M>;
   constexpr int HX = Gm::HX, HY = Gm::HY, PX = Gm::PX, FSZ = Gm::FSZ, NPT = Gm::NPT, TP = Gm::TP;
+  constexpr int XO = Gm::XO, XC = Gm::XC;  // staged column offsets (odd m)
   extern __shared__ double SM[];
   double *PR = SM + Gm::OFF_PR;
   double *E0 = SM + Gm::OFF_E0, *E1 = SM + Gm::OFF_E1;
@@ -599,11 +620,11 @@ OSBLI_UNROLL(OSBLI_XY_FORM_UNROLL)
       {
         const int row = q7 & 15, seg = q7 >> 4;
         const int hy = row + M;
-        const int base = hy * PX + seg * XY_RX;  // window start (halo coords)
+        const int base = hy * PX + seg * XY_RX + XO;  // window start (staged coords)
         const int pt0 = row * TP + seg * XY_RX;
         VelResult<M> o;
         velocity_dir<M, 0, VAR, MIXB>(
-            p, S, PR, base, 1, G02 + row * PX + seg * XY_RX, 1, E0, E1, 0, o);
+            p, S, PR, base, 1, G02 + row * PX + seg * XY_RX + XO, 1, E0, E1, 0, o);
         // B has finished reading XA (its epilogue of the previous plane)
         if (i > 0) nbar_sync(10, XY_THREADS);
         if (OSBLI_DEBUG_CHECKS) {
@@ -652,13 +673,13 @@ OSBLI_UNROLL(OSBLI_XY_FORM_UNROLL)
       for (int task = q7; task < 2 * M * (XY_TX / XY_RX); task += 128) {
         const int rr = task % (2 * M), seg = task / (2 * M);
         const int hy = rr < M ? rr : rr + XY_TY;
-        const int base = hy * PX + seg * XY_RX;
+        const int base = hy * PX + seg * XY_RX + XO;
         constexpr int W = Gm::W;
         double r[W], v[W], t[W];
-        ldwin<W, Gm::PAIRS>(PR + XP_R * FSZ + base, 1, r);
+        ldwin<W, Gm::XW>(PR + XP_R * FSZ + base, 1, r);
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
-          ldwin<W, Gm::PAIRS>(S + (XF_M0 + i) * FSZ + base, 1, t);
+          ldwin<W, Gm::XW>(S + (XF_M0 + i) * FSZ + base, 1, t);
 #pragma unroll
           for (int k = 0; k < W; ++k) v[k] = __dmul_rn(t[k], r[k]);
           double *Ei = i == 0 ? E0 : E1;
@@ -670,7 +691,7 @@ OSBLI_UNROLL(OSBLI_XY_FORM_UNROLL)
       // ---- phase Y: thread -> (column, 4-tall y segment); lanes = 32 consecutive columns
       {
         const int col = q7 & 31, seg = q7 >> 5;
-        const int base = (seg * XY_RY) * PX + col + M;
+        const int base = (seg * XY_RY) * PX + col + XC;
         const int ebase = (seg * XY_RY) * TP + col;
         const int gbase = (seg * XY_RY) * Gm::GP + col;
         double dTz[4];
@@ -690,11 +711,11 @@ OSBLI_UNROLL(OSBLI_XY_FORM_UNROLL)
           for (int j = 0; j < 4; ++j) {
             const int ty = seg * XY_RY + j;
             const int pt = ty * TP + col;
-            const int c = (ty + M) * PX + col + M;
+            const int c = (ty + M) * PX + col + XC;
             const double g00 = E0[(ty + M) * TP + col], g10 = E1[(ty + M) * TP + col];
             const double g20 = XA[4 * NPT + pt];
             const double g01 = o.g[0][j], g11 = o.g[1][j], g21 = o.g[2][j];
-            const double g02 = G02[ty * PX + col + M], g12 = G12[(ty + M) * Gm::GP + col],
+            const double g02 = G02[ty * PX + col + XC], g12 = G12[(ty + M) * Gm::GP + col],
                          g22 = S[XF_G22 * FSZ + c];
             const double T = o.Tc[j];
             const double mu = p.visc ? sutherland_mu(p, T) : 1.0;
@@ -752,11 +773,11 @@ OSBLI_UNROLL(OSBLI_XY_FORM_UNROLL)
         for (int j = 0; j < 4; ++j) {
           const int ty = seg * XY_RY + j;
           const int pt = ty * TP + col;
-          const int c = (ty + M) * PX + col + M;
+          const int c = (ty + M) * PX + col + XC;
           const double g00 = E0[(ty + M) * TP + col], g10 = E1[(ty + M) * TP + col];
           const double g20 = XA[4 * NPT + pt];
           const double g01 = o.g[0][j], g11 = o.g[1][j], g21 = o.g[2][j];
-          const double g02 = G02[ty * PX + col + M], g12 = G12[(ty + M) * Gm::GP + col],
+          const double g02 = G02[ty * PX + col + XC], g12 = G12[(ty + M) * Gm::GP + col],
                        g22 = S[XF_G22 * FSZ + c];
           // y-parts of V_i: V0 += nu (D11 u0 + 1/3 D1 g10);
           // V1 += nu (4/3 D11 u1 + 1/3 (D1 g00 + D1 g22)); V2 += nu (D11 u2 + 1/3 D1 g12)
@@ -807,7 +828,7 @@ OSBLI_UNROLL(OSBLI_XY_FORM_UNROLL)
       // ---- phase X: x-derivatives of the conservative group
       {
         const int row = q7 & 15, seg = q7 >> 4;
-        const int base = (row + M) * PX + seg * XY_RX;
+        const int base = (row + M) * PX + seg * XY_RX + XO;
         const int pt0 = row * TP + seg * XY_RX;
         double R[5][4];
         conservative_dir<M, 0, !VAR>(p, S, PR, base, 1, R);
@@ -816,10 +837,10 @@ OSBLI_UNROLL(OSBLI_XY_FORM_UNROLL)
           // nu/3 D_x g02 (momentum z), and their work u_i V_i (D-7)
           constexpr int W = Gm::W;
           double v[W], ma[4];
-          ldwin<W, Gm::PAIRS>(S + XF_G22 * FSZ + base, 1, v);
+          ldwin<W, Gm::XW>(S + XF_G22 * FSZ + base, 1, v);
 #pragma unroll
           for (int j = 0; j < 4; ++j) ma[j] = (p.nu * third) * wd1<M, W>(p, v, j);
-          ldwin<W, Gm::PAIRS>(S + Gm::PB_G02 + row * PX + seg * XY_RX, 1, v);
+          ldwin<W, Gm::XW>(S + Gm::PB_G02 + row * PX + seg * XY_RX + XO, 1, v);
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             const double mb = (p.nu * third) * wd1<M, W>(p, v, j);
@@ -839,7 +860,7 @@ OSBLI_UNROLL(OSBLI_XY_FORM_UNROLL)
       // ---- phase Y and the epilogue
       {
         const int col = q7 & 31, seg = q7 >> 5;
-        const int base = (seg * XY_RY) * PX + col + M;
+        const int base = (seg * XY_RY) * PX + col + XC;
         // group B finishes the stage for its 4 points: W' (z-pass output) is loaded
         // first so that its latency hides behind the y-derivatives
         const int x = x0 + col;
@@ -909,7 +930,7 @@ OSBLI_UNROLL(OSBLI_XY_FORM_UNROLL)
             const int ty = seg * XY_RY + j;
             const int y = y0 + ty;
             if (!xin || y >= p.ny) continue;
-            store(j, (ty + M) * PX + col + M, (size_t)z * 5 * FS + (size_t)y * p.nx + x,
+            store(j, (ty + M) * PX + col + XC, (size_t)z * 5 * FS + (size_t)y * p.nx + x,
                   qout + qplane(p, z) + (size_t)y * p.nx + x);
           }
         };

@@ -26,6 +26,9 @@ constexpr int ZP_TX = 32;
 #ifndef OSBLI_ZP_ADV_UNROLL
 #define OSBLI_ZP_ADV_UNROLL 4
 #endif
+#ifndef OSBLI_ZP_PERSIST
+#define OSBLI_ZP_PERSIST 0
+#endif
 #ifndef OSBLI_ZP_MINB
 #define OSBLI_ZP_MINB 1
 #endif
@@ -149,9 +152,16 @@ __global__ void __launch_bounds__(ZP_THREADS, OSBLI_ZP_MINB)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // blockIdx.x enumerates (x-tile, y-row) pencils (grid.y would cap ny at 65535)
   const int gx = (p.nx + ZP_TX - 1) / ZP_TX;
-  const int x0 = (int)(blockIdx.x % gx) * ZP_TX, y = (int)(blockIdx.x / gx);
   int zs, ze;
   if (!zr.segment(zs, ze)) return;
+#if OSBLI_ZP_PERSIST
+  // experiment: a grid smaller than the pencil count loops over the pencils
+  for (unsigned pen = blockIdx.x; pen < (unsigned)(gx * p.ny); pen += gridDim.x) {
+  __syncthreads();
+  const int x0 = (int)(pen % gx) * ZP_TX, y = (int)(pen / gx);
+#else
+  const int x0 = (int)(blockIdx.x % gx) * ZP_TX, y = (int)(blockIdx.x / gx);
+#endif
   const int nchunks = (ze - zs + ZP_TZ - 1) / ZP_TZ;
   const size_t FS = (size_t)p.nx * p.ny;
   // column this thread loads for staging slot c = tid & 31 (ragged tiles load any valid column)
@@ -361,4 +371,7 @@ OSBLI_UNROLL(OSBLI_ZP_ADV_UNROLL)
       if (k + 2 < nchunks) issue_raw(k + 2);
     }
   }
+#if OSBLI_ZP_PERSIST
+  }
+#endif
 }
