@@ -96,18 +96,24 @@ def run_scalar(args, cfg):
     x = np.arange(n) * dx
     Z, Y, X = np.meshgrid(x, x, x, indexing="ij")
     s.set_state(np.ascontiguousarray(np.sin(X) * np.cos(Y) * np.cos(Z)))
-    for _ in range(args.warmup):
-        s.step(1)
-    s.sync()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if world > 1:
-        torch.distributed.barrier()
-    torch.cuda.synchronize()
-    e0.record(stream)
-    s.step(args.steps)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    s.sync()
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        # warm-up of at least W steps and 1 s (the clock sampler's start-up)
+        t_w = time.perf_counter()
+        while True:
+            for _ in range(args.warmup):
+                s.step(1)
+            s.sync()
+            if time.perf_counter() - t_w > 1.0:
+                break
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        s.step(args.steps)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        s.sync()
     ms = e0.elapsed_time(e1)
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
@@ -131,6 +137,7 @@ def run_scalar(args, cfg):
                      "frac": achieved / float(peaks["hbm_gbs"]), "traffic": None,
                      "bytes_per_point_step": bytes_step,
                      "timing": "CUDA events on the solver stream"},
+        "clocks": clk.summary(),
         "gpu_launches": 3 * args.steps,
     }), flush=True)
 
