@@ -368,17 +368,21 @@ cudaError_t xypass_launch(const KParams &p, const double *q, double *qout, doubl
                           const double *gz, double *rout, unsigned int *flag, int zb, int ze,
                           int zb1, int ze1, cudaStream_t s) {
   constexpr int smem = ws::xy_smem_bytes<M>();
-  // the five instantiations of the stepping paths, then the same with fused diagnostics
-  const int v = ((p.visc || p.cons) ? 4 : (p.two_reg ? 1 : 0) + (p.sym[0] || p.sym[1] ? 2 : 0)) +
-                (p.dpart ? 5 : 0);
+  // the six instantiations of the stepping paths (default, two-register, symmetric,
+  // both, equation variants, variants with the two-register epilogue), then the same
+  // with fused diagnostics
+  const int tr = p.two_reg ? 1 : 0;
+  const int v = ((p.visc || p.cons) ? 4 + tr : tr + (p.sym[0] || p.sym[1] ? 2 : 0)) +
+                (p.dpart ? 6 : 0);
   using K = decltype(&ws::xypass_kernel<M, 0>);
-  static const K kerns[10] = {ws::xypass_kernel<M, 0>,  ws::xypass_kernel<M, 1>,
+  static const K kerns[12] = {ws::xypass_kernel<M, 0>,  ws::xypass_kernel<M, 1>,
                               ws::xypass_kernel<M, 2>,  ws::xypass_kernel<M, 3>,
-                              ws::xypass_kernel<M, 4>,  ws::xypass_kernel<M, 8>,
-                              ws::xypass_kernel<M, 9>,  ws::xypass_kernel<M, 10>,
-                              ws::xypass_kernel<M, 11>, ws::xypass_kernel<M, 12>};
+                              ws::xypass_kernel<M, 4>,  ws::xypass_kernel<M, 5>,
+                              ws::xypass_kernel<M, 8>,  ws::xypass_kernel<M, 9>,
+                              ws::xypass_kernel<M, 10>, ws::xypass_kernel<M, 11>,
+                              ws::xypass_kernel<M, 12>, ws::xypass_kernel<M, 13>};
   const K kern = kerns[v];
-  static unsigned done[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  static unsigned done[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   cudaError_t e = ensure_smem_attr(kern, smem, done[v]);
   if (e != cudaSuccess) return e;
   // planes per CTA: xy_seg<M>, halved while the grid would not cover the SMs (small grids)

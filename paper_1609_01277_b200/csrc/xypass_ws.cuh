@@ -505,7 +505,8 @@ __device__ __forceinline__ void diag_tile_sum(const KParams &p, double (&dg)[3],
 // TR (1): two-register RK3 epilogue (OSBLI_RK3_2R, kernels.h): W' is read from
 //   the interior planes of qout (where the z-pass left it) and w holds Q_old.
 // VAR (4): mu(T) (grad-mu terms from D_x T, D_y T and the z-pass's D_z T) and the
-//   conservative viscous work (H_j written for launch_divh); TR and SYM at run time.
+//   conservative viscous work (H_j written for launch_divh); SYM at run time (with
+//   the two-register epilogue: XF = 5).
 template <int M, int XF>
 __global__ void __launch_bounds__(XY_CTA, 1)
     xypass_kernel(const KParams p, const double *__restrict__ q, double *__restrict__ qout,
@@ -513,12 +514,12 @@ __global__ void __launch_bounds__(XY_CTA, 1)
                   double *__restrict__ rout,
                   unsigned int *__restrict__ flag, const PlaneRange zr) {
   // XF bits: 1 = two-register epilogue, 2 = symmetry in x/y, 4 = equation variants
-  // (mu(T), conservative viscous work), which take the other two at run time;
+  // (mu(T), conservative viscous work), which take symmetry at run time;
   // 8 = fused diagnostics (stage 1 of osbli_step_diag)
   constexpr bool VAR = (XF & 4) != 0;
   constexpr bool DIAG = (XF & 8) != 0;  // fused diagnostics into p.dpart (osbli_step_diag)
   constexpr bool SYM = VAR || (XF & 2) != 0;
-  const bool TR = VAR ? p.two_reg != 0 : (XF & 1) != 0;
+  constexpr bool TR = (XF & 1) != 0;
   // group B takes the x mixed-derivative parts (XY_MIXX_B) in the default and
   // diagnostics instantiations; the two-register epilogue holds Q_old in B's
   // registers, and there the move would spill
@@ -560,6 +561,9 @@ __global__ void __launch_bounds__(XY_CTA, 1)
     int *cx = reinterpret_cast<int *>(SM + Gm::TOTAL), *ry = cx + Gm::HX;
     xy_tables<M, SYM>(p, cx, ry, x0, y0, lane, XY_PROD);
     nbar_sync(7, XY_PROD);  // tables complete (producers only)
+    // 16-byte x-pairs (even nx, periodic x).  The symmetric instantiation stages 8
+    // bytes at a time everywhere: a mirrored pair is reversed in memory, and pairs
+    // on its interior tiles only measured slower (1.63 vs 1.55 ms at 256^3 o12)
     const bool pairs = !SYM && (p.nx % 2) == 0;
     for (int i = 0; i < nplanes; ++i) {
       const int b = i & 1;
