@@ -28,7 +28,13 @@
 // This translation unit instantiates every order-dependent kernel for one
 // stencil half width M = OSBLI_M (the Makefile compiles it once per M, in
 // parallel); kernels.cu dispatches on the run-time order.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdint>
 #include <cstdlib>
+#include <cstring>
+#include <mutex>
 
 #include "device_common.cuh"
 #include "dispatch.h"
@@ -333,6 +339,66 @@ inline bool no_split() {
   return v != 0;
 }
 
+// TMA tensor map of a Q buffer, [nz + 2G][5][ny][nx] fp64 as a 4-D tensor (x, y, field,
+// plane) with a (32, 1, 5, 1) box: one z-pass staging plane of a pencil.  Built once
+// per buffer (a small cache keyed by the buffer and its shape); nullptr when TMA does
+// not apply (odd nx: row strides must be multiples of 16 bytes) or the driver entry
+// point is missing, and the z-pass then stages with cp.async.
+const CUtensorMap *qbuf_tensor_map(const double *q, const KParams &p) {
+  if (p.nx % 2 != 0 || p.nx < 32) return nullptr;
+  static std::mutex mu;
+  static PFN_cuTensorMapEncodeTiled encode = nullptr;
+  static bool tried = false;
+  struct Entry {
+    const double *q;
+    int nx, ny, planes;
+    CUtensorMap map;
+  };
+  static Entry cache[16];
+  static int next = 0;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!tried) {
+    tried = true;
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr) ==
+            cudaSuccess &&
+        qr == cudaDriverEntryPointSuccess)
+      encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
+  }
+  if (!encode) return nullptr;
+  const int planes = p.nz + 2 * p.G;
+  for (const Entry &e : cache)
+    if (e.q == q && e.nx == p.nx && e.ny == p.ny && e.planes == planes) return &e.map;
+  Entry &e = cache[next];
+  next = (next + 1) % 16;
+  const cuuint64_t dims[4] = {(cuuint64_t)p.nx, (cuuint64_t)p.ny, 5, (cuuint64_t)planes};
+  const cuuint64_t strides[3] = {(cuuint64_t)p.nx * 8, (cuuint64_t)p.nx * p.ny * 8,
+                                 (cuuint64_t)5 * p.nx * p.ny * 8};
+  const cuuint32_t box[4] = {ZP_TX, 1, 5, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  if (encode(&e.map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double *>(q), dims, strides,
+             box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+    e.q = nullptr;
+    return nullptr;
+  }
+  e.q = q;
+  e.nx = p.nx;
+  e.ny = p.ny;
+  e.planes = planes;
+  return &e.map;
+}
+
+// OSBLI_ZP_TMA=0 (testing): stage the z-pass with cp.async everywhere
+inline bool zp_tma_enabled() {
+  static const bool v = [] {
+    const char *e = std::getenv("OSBLI_ZP_TMA");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
 template <int M>
 cudaError_t zpass_launch(const KParams &p, const double *q, double *w, double *gz, int zb, int ze,
                          int zb1, int ze1, cudaStream_t s) {
@@ -359,7 +425,10 @@ cudaError_t zpass_launch(const KParams &p, const double *q, double *w, double *g
     if (g > 0 && g < gx * gy) grid.x = g;
   }
 #endif
-  kern<<<grid, ZP_THREADS, smem, s>>>(p, q, w, gz, zr);
+  const CUtensorMap *tm = zp_tma_enabled() ? qbuf_tensor_map(q, p) : nullptr;
+  CUtensorMap none;
+  std::memset(&none, 0, sizeof(none));
+  kern<<<grid, ZP_THREADS, smem, s>>>(p, q, w, gz, zr, tm ? *tm : none, tm ? 1 : 0);
   return cudaGetLastError();
 }
 

@@ -14,8 +14,11 @@
 // plane): consecutive chunks share their 2m overlap planes, so every
 // plane is loaded from HBM once.  While chunk k is computed, the raw state of
 // the TZ planes chunk k+1 adds is already in flight into a staging buffer
-// (cp.async), so the HBM latency hides behind the FP64 work.  Each thread
-// produces RZ = 4 consecutive z outputs of its column from register windows.
+// (TMA: one 32-column x 5-field tensor box per plane, cp.async.bulk.tensor into
+// an mbarrier, issued by the 32 lanes of warp 0; cp.async where the pencil is
+// ragged or nx is odd), so the HBM latency hides behind the FP64 work.  Each
+// thread produces RZ = 4 consecutive z outputs of its column from register
+// windows.
 constexpr int ZP_TX = 32;
 #ifndef OSBLI_ZP_TZ
 #define OSBLI_ZP_TZ 32
@@ -42,10 +45,43 @@ enum { ZS_RHO = 0, ZS_M0, ZS_M1, ZS_M2, ZS_E, ZS_U0, ZS_U1, ZS_U2, ZS_T, ZS_F0, 
 template <int M>
 struct ZGeom {
   static constexpr int NR = ZP_TZ + 2 * M;      // ring slots (planes)
-  static constexpr int RING = ZP_NF * NR * 32;  // doubles
-  static constexpr int RAW = 5 * ZP_TZ * 32;    // raw planes of the next chunk
-  static constexpr int BYTES = (RING + RAW) * (int)sizeof(double);
+  static constexpr int RING = ZP_NF * NR * 32;  // doubles (a multiple of 16: RAW is 128-B aligned)
+  static constexpr int RAW = 5 * ZP_TZ * 32;    // raw planes of the next chunk, [plane][field][32]
+  // + the TMA mbarrier (8 bytes, padded to 16)
+  static constexpr int BYTES = (RING + RAW) * (int)sizeof(double) + 16;
 };
+static_assert((ZP_NF * 32) % 16 == 0, "the raw staging buffer must stay 128-byte aligned");
+
+// TMA: bulk tensor copy of one box of the Q buffer (tensor map over [planes][5][ny][nx])
+// into shared memory, completing on an mbarrier
+__device__ __forceinline__ void tma_load_plane(double *dst, const CUtensorMap *tm, int x, int y,
+                                               int zplane, uint64_t *bar) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::"r"(d),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(0), "r"(zplane), "r"(b)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(b), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(b), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "{\n .reg .pred P;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+      " @!P bra WAIT_%=;\n}\n" ::"r"(b), "r"(parity)
+      : "memory");
+}
 
 template <int M>
 constexpr int zp_smem_bytes() {
@@ -142,13 +178,16 @@ __device__ __forceinline__ double d2w(const KParams &p, const double (&v)[ZP_RZ 
 template <int M, int ZF>
 __global__ void __launch_bounds__(ZP_THREADS, OSBLI_ZP_MINB)
     zpass_kernel(const KParams p, const double *__restrict__ q, double *__restrict__ w,
-                 double *__restrict__ gz, const PlaneRange zr) {
+                 double *__restrict__ gz, const PlaneRange zr,
+                 const __grid_constant__ CUtensorMap tmq, const int use_tma) {
   constexpr bool SYMZ = ZF != 0;
   constexpr bool VAR = ZF == 2;
   using Zg = ZGeom<M>;
   constexpr int NR = Zg::NR;
-  extern __shared__ double S[];
+  extern __shared__ __align__(128) double S[];
   double *RB = S + Zg::RING;
+  uint64_t *tbar = reinterpret_cast<uint64_t *>(RB + Zg::RAW);
+  unsigned tphase = 0;  // completed TMA phases of tbar
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // blockIdx.x enumerates (x-tile, y-row) pencils (grid.y would cap ny at 65535)
   const int gx = (p.nx + ZP_TX - 1) / ZP_TX;
@@ -196,11 +235,31 @@ __global__ void __launch_bounds__(ZP_THREADS, OSBLI_ZP_MINB)
                   raw[it][4]);
     }
   }
-  // raw planes of chunk kk: z = zs + kk*TZ + M + j, j = 0..TZ-1  ->  RB[f][j][c]
-  // 16-byte copies of column pairs when the pencil lies inside the grid and rows
-  // start at even offsets (even nx: no pair straddles the periodic wrap)
+  // raw planes of chunk kk: z = zs + kk*TZ + M + j, j = 0..TZ-1  ->  RB[j][f][c]
+  // TMA boxes (or 16-byte copies of column pairs) when the pencil lies inside the
+  // grid and rows start at even offsets (even nx: no pair straddles the periodic wrap)
   const bool pairs = (p.nx % 2) == 0 && x0 + ZP_TX <= p.nx;
+  const bool tma = use_tma && pairs && !OSBLI_DEBUG_CHECKS;
+  if (tma) {
+    if (tid == 0) mbar_init(tbar, 1);
+    tphase = 0;
+  }
   auto issue_raw = [&](int kk) {
+    if (tma) {
+      // lanes 0..RZ-1 of every warp issue one plane box each (the issue of a warp's
+      // TMA instructions is serial, so it is spread over the warps); a copy may
+      // complete before the expect-tx: the phase still needs the one arrival
+      if (tid == 0) mbar_expect_tx(tbar, ZP_TZ * 5 * 32 * (unsigned)sizeof(double));
+      constexpr int PW = ZP_TZ / (ZP_THREADS / 32);  // planes per warp
+      if (lane < PW) {
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        const int j = warp * PW + lane;
+        int fl_;
+        const int zb_ = zread_t<SYMZ>(p, zs + kk * ZP_TZ + M + j, fl_) + p.G;
+        tma_load_plane(RB + j * 5 * 32, &tmq, x0, y, zb_, tbar);
+      }
+      return;
+    }
     if (pairs) {
       // lanes 0-15: plane j, columns 2l, 2l+1; lanes 16-31: plane j + 1
       const int l2 = 2 * (lane & 15);
@@ -212,7 +271,7 @@ __global__ void __launch_bounds__(ZP_THREADS, OSBLI_ZP_MINB)
                                     dbg_in(p, qp - q + 4 * FS + 1, qbuf_len(p))))
           qp = q;
 #pragma unroll
-        for (int f = 0; f < 5; ++f) cp_async16z(RB + (f * ZP_TZ + idx) * 32 + l2, qp + f * FS);
+        for (int f = 0; f < 5; ++f) cp_async16z(RB + (idx * 5 + f) * 32 + l2, qp + f * FS);
       }
     } else {
       for (int idx = tid; idx < ZP_TZ * 32; idx += ZP_THREADS) {
@@ -223,11 +282,12 @@ __global__ void __launch_bounds__(ZP_THREADS, OSBLI_ZP_MINB)
                                     dbg_in(p, qp - q + 4 * FS, qbuf_len(p))))
           qp = q;
 #pragma unroll
-        for (int f = 0; f < 5; ++f) cp_async8(RB + (f * ZP_TZ + j) * 32 + lane, qp + f * FS);
+        for (int f = 0; f < 5; ++f) cp_async8(RB + (j * 5 + f) * 32 + lane, qp + f * FS);
       }
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
+  __syncthreads();  // the mbarrier is initialised
   if (nchunks > 1) issue_raw(1);
   __syncthreads();
 
@@ -352,7 +412,12 @@ __global__ void __launch_bounds__(ZP_THREADS, OSBLI_ZP_MINB)
     }
     if (k + 1 < nchunks) {
       // ---- advance the ring: planes of chunk k+1 replace the first TZ planes of chunk k
-      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      if (tma) {
+        mbar_wait(tbar, tphase & 1);
+        ++tphase;
+      } else {
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      }
       __syncthreads();  // staged raw planes visible; every warp is done with chunk k
       // unrolled: the loads of all its points are in flight together (ZP_TZ*32 is a
       // multiple of the block size)
@@ -362,10 +427,9 @@ OSBLI_UNROLL(OSBLI_ZP_ADV_UNROLL)
         const int slot = ((k + 1) * ZP_TZ + 2 * M + j) % NR;
         int fl = 0;
         if (SYMZ) zread(p, zs + (k + 1) * ZP_TZ + M + j, fl);
-        const double m2 = RB[(3 * ZP_TZ + j) * 32 + lane];
-        zstore<M>(p, S, slot, lane, RB[(0 * ZP_TZ + j) * 32 + lane],
-                  RB[(1 * ZP_TZ + j) * 32 + lane], RB[(2 * ZP_TZ + j) * 32 + lane],
-                  fl ? -m2 : m2, RB[(4 * ZP_TZ + j) * 32 + lane]);
+        const double *rb = RB + j * 5 * 32 + lane;
+        const double m2 = rb[3 * 32];
+        zstore<M>(p, S, slot, lane, rb[0], rb[32], rb[2 * 32], fl ? -m2 : m2, rb[4 * 32]);
       }
       __syncthreads();  // ring updated, staging buffer free
       if (k + 2 < nchunks) issue_raw(k + 2);
