@@ -2,6 +2,8 @@
 // index maps, cp.async, fast reciprocals, Sutherland).  Internal linkage: every
 // translation unit gets its own copy.
 #pragma once
+#include <cuda.h>
+
 #include <cstdint>
 
 #include "kernels.h"
@@ -184,4 +186,36 @@ __device__ __forceinline__ double sutherland_dmu(const KParams &p, double T, dou
 #define OSBLI_D2_SBP 1
 #endif
 }  // namespace
+// TMA: bulk tensor copy of one box of a 4-D tensor (x, y, field, plane) into shared
+// memory (128-byte aligned), completing on an mbarrier
+__device__ __forceinline__ void tma_load_box(double *dst, const CUtensorMap *tm, int x, int y,
+                                             int f, int zplane, uint64_t *bar) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::"r"(d),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(f), "r"(zplane), "r"(b)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(b), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(b), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "{\n .reg .pred P;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+      " @!P bra WAIT_%=;\n}\n" ::"r"(b), "r"(parity)
+      : "memory");
+}
+
+
 }  // namespace osbli

@@ -339,22 +339,23 @@ inline bool no_split() {
   return v != 0;
 }
 
-// TMA tensor map of a Q buffer, [nz + 2G][5][ny][nx] fp64 as a 4-D tensor (x, y, field,
-// plane) with a (32, 1, 5, 1) box: one z-pass staging plane of a pencil.  Built once
-// per buffer (a small cache keyed by the buffer and its shape); nullptr when TMA does
-// not apply (odd nx: row strides must be multiples of 16 bytes) or the driver entry
-// point is missing, and the z-pass then stages with cp.async.
-const CUtensorMap *qbuf_tensor_map(const double *q, const KParams &p) {
-  if (p.nx % 2 != 0 || p.nx < 32) return nullptr;
+// TMA tensor maps of the solver's buffers, as 4-D fp64 tensors (x, y, field, plane):
+// Q buffers [nz + 2G][5][ny][nx] and Gz [nz][3][ny][nx].  Built once per (buffer,
+// shape, box) (a small cache); nullptr when TMA does not apply (odd nx: row strides
+// must be multiples of 16 bytes) or the driver entry point is missing, and the
+// kernels then stage with cp.async.
+const CUtensorMap *tensor_map(const double *ptr, int nx, int ny, int nf, int planes, int bx,
+                              int by, int bf) {
+  if (nx % 2 != 0) return nullptr;
   static std::mutex mu;
   static PFN_cuTensorMapEncodeTiled encode = nullptr;
   static bool tried = false;
   struct Entry {
-    const double *q;
-    int nx, ny, planes;
+    const double *ptr;
+    int key[7];
     CUtensorMap map;
   };
-  static Entry cache[16];
+  static Entry cache[32];
   static int next = 0;
   std::lock_guard<std::mutex> lock(mu);
   if (!tried) {
@@ -367,35 +368,44 @@ const CUtensorMap *qbuf_tensor_map(const double *q, const KParams &p) {
       encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
   }
   if (!encode) return nullptr;
-  const int planes = p.nz + 2 * p.G;
+  const int key[7] = {nx, ny, nf, planes, bx, by, bf};
   for (const Entry &e : cache)
-    if (e.q == q && e.nx == p.nx && e.ny == p.ny && e.planes == planes) return &e.map;
+    if (e.ptr == ptr && std::memcmp(e.key, key, sizeof(key)) == 0) return &e.map;
   Entry &e = cache[next];
-  next = (next + 1) % 16;
-  const cuuint64_t dims[4] = {(cuuint64_t)p.nx, (cuuint64_t)p.ny, 5, (cuuint64_t)planes};
-  const cuuint64_t strides[3] = {(cuuint64_t)p.nx * 8, (cuuint64_t)p.nx * p.ny * 8,
-                                 (cuuint64_t)5 * p.nx * p.ny * 8};
-  const cuuint32_t box[4] = {ZP_TX, 1, 5, 1};
+  next = (next + 1) % 32;
+  const cuuint64_t dims[4] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)nf, (cuuint64_t)planes};
+  const cuuint64_t strides[3] = {(cuuint64_t)nx * 8, (cuuint64_t)nx * ny * 8,
+                                 (cuuint64_t)nf * nx * ny * 8};
+  const cuuint32_t box[4] = {(cuuint32_t)bx, (cuuint32_t)by, (cuuint32_t)bf, 1};
   const cuuint32_t estr[4] = {1, 1, 1, 1};
-  if (encode(&e.map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double *>(q), dims, strides,
+  if (encode(&e.map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double *>(ptr), dims, strides,
              box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
-    e.q = nullptr;
+    e.ptr = nullptr;
     return nullptr;
   }
-  e.q = q;
-  e.nx = p.nx;
-  e.ny = p.ny;
-  e.planes = planes;
+  e.ptr = ptr;
+  std::memcpy(e.key, key, sizeof(key));
   return &e.map;
 }
 
-// OSBLI_ZP_TMA=0 (testing): stage the z-pass with cp.async everywhere
+// z-pass staging box: one plane of a 32-column pencil, all five fields
+const CUtensorMap *qbuf_tensor_map(const double *q, const KParams &p) {
+  if (p.nx < ZP_TX) return nullptr;
+  return tensor_map(q, p.nx, p.ny, 5, p.nz + 2 * p.G, ZP_TX, 1, 5);
+}
+
+// OSBLI_ZP_TMA=0 / OSBLI_XY_TMA=0 (testing): stage the z-pass / xy-pass with cp.async everywhere
+inline bool env_on(const char *name) {
+  const char *e = std::getenv(name);
+  return !(e && e[0] == '0');
+}
 inline bool zp_tma_enabled() {
-  static const bool v = [] {
-    const char *e = std::getenv("OSBLI_ZP_TMA");
-    return !(e && e[0] == '0');
-  }();
+  static const bool v = env_on("OSBLI_ZP_TMA");
+  return v;
+}
+inline bool xy_tma_enabled() {
+  static const bool v = env_on("OSBLI_XY_TMA");
   return v;
 }
 
@@ -464,7 +474,20 @@ cudaError_t xypass_launch(const KParams &p, const double *q, double *qout, doubl
   int ntot = 0;
   const PlaneRange zr = plane_range(zb, ze, zb1, ze1, seg, &ntot);
   dim3 grid((p.nx + ws::XY_TX - 1) / ws::XY_TX, (p.ny + ws::XY_TY - 1) / ws::XY_TY, ntot);
-  kern<<<grid, ws::XY_CTA, smem, s>>>(p, q, qout, w, gz, rout, flag, zr);
+  using Gm = ws::XYGeom<M>;
+  const CUtensorMap *tq = nullptr, *t22 = nullptr, *t02 = nullptr, *t12 = nullptr;
+  if (xy_tma_enabled() && p.nx >= Gm::PX && p.ny >= Gm::HY) {
+    tq = tensor_map(q, p.nx, p.ny, 5, p.nz + 2 * p.G, Gm::PX, Gm::HY, 5);
+    t22 = tensor_map(gz, p.nx, p.ny, 3, p.nz, Gm::PX, Gm::HY, 1);
+    t02 = tensor_map(gz, p.nx, p.ny, 3, p.nz, Gm::PX, ws::XY_TY, 1);
+    t12 = tensor_map(gz, p.nx, p.ny, 3, p.nz, Gm::GP, Gm::HY, 1);
+  }
+  const bool tma = tq && t22 && t02 && t12;
+  CUtensorMap none;
+  std::memset(&none, 0, sizeof(none));
+  kern<<<grid, ws::XY_CTA, smem, s>>>(p, q, qout, w, gz, rout, flag, zr, tma ? *tq : none,
+                                      tma ? *t22 : none, tma ? *t02 : none, tma ? *t12 : none,
+                                      tma ? 1 : 0);
   return cudaGetLastError();
 }
 

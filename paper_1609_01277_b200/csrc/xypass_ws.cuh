@@ -87,7 +87,7 @@ template <int M>
 constexpr int xy_seg() { return OSBLI_XY_SEG; }
 #endif
 // full-halo fields of a plane buffer (S) and of the per-plane formula arrays (PR)
-enum { XF_RHO = 0, XF_M0, XF_M1, XF_M2, XF_E, XF_G22, XF_N };
+enum { XF_RHO = 0, XF_M0, XF_M1, XF_M2, XF_E };
 enum { XP_P = 0, XP_R = 1 };
 
 template <int M>
@@ -113,10 +113,14 @@ struct XYGeom {
   static constexpr int EXT = TP * HY;       // tile columns x (tile + y-halo) rows
   static constexpr int W = 4 + 2 * M;       // window length (RX = RY = 4)
   static constexpr int GP = XY_TX;          // pitch of the g12 strip (column-per-lane access)
-  // plane buffer (doubles): 6 full-halo fields | g02 [TY][PX] (tile rows) | g12 [HY][GP] (tile cols)
-  static constexpr int PB_G02 = XF_N * FSZ;
-  static constexpr int PB_G12 = PB_G02 + XY_TY * PX;
-  static constexpr int PBSZ = PB_G12 + HY * GP;
+  // plane buffer (doubles): rho, m_i, e [5][HY][PX] | g22 [HY][PX] | g02 [TY][PX] (tile
+  // rows) | g12 [HY][GP] (tile cols); each part starts on a 128-byte boundary (a TMA
+  // destination: the first is one 5-field box, the others one box each)
+  static constexpr int al16(int n) { return (n + 15) / 16 * 16; }
+  static constexpr int PB_G22 = al16(5 * FSZ);
+  static constexpr int PB_G02 = al16(PB_G22 + FSZ);
+  static constexpr int PB_G12 = al16(PB_G02 + XY_TY * PX);
+  static constexpr int PBSZ = al16(PB_G12 + HY * GP);
   // layout: PB[2] | PR (p, r) | E0 | E1 | XA[5] | XB[5] | XT
   static constexpr int OFF_PR = 2 * PBSZ;
   static constexpr int OFF_E0 = OFF_PR + 2 * FSZ;   // [HY][TP]   g00 (y-extended)
@@ -125,7 +129,8 @@ struct XYGeom {
   static constexpr int OFF_XB = OFF_XA + 5 * NPT;   // 5 x [TY][TP]
   static constexpr int OFF_XT = OFF_XB + 5 * NPT;   // [TY][TP] D_x T (equation variants)
   static constexpr int OFF_DG = OFF_XT + NPT;       // [4 warps][3] fused diagnostics partials
-  static constexpr int TOTAL = OFF_DG + 16;
+  static constexpr int OFF_BAR = OFF_DG + 16;       // 2 TMA mbarriers (plane buffers)
+  static constexpr int TOTAL = OFF_BAR + 2;
   // producer gather tables (ints): global x of each halo column, y * nx of each halo row
   static constexpr int TAB_INTS = HX + HY;
   static constexpr int BYTES = TOTAL * (int)sizeof(double) + TAB_INTS * (int)sizeof(int);
@@ -252,7 +257,7 @@ __device__ __forceinline__ void velocity_dir(const KParams &p, const double *S, 
     }
   }
   if (!NOMIX) {
-    ldwin<W, PW>(S + XF_G22 * Gm::FSZ + base, st, v);  // D_d g22
+    ldwin<W, PW>(S + Gm::PB_G22 + base, st, v);  // D_d g22
 #pragma unroll
     for (int j = 0; j < 4; ++j) o.mixA[j] = wd1<M, W>(p, v, j);
     ldwin<W, PW>(gmix, gst, v);  // DIR 0: D_x g02 = D_z g00 ; DIR 1: D_y g12 = D_z g11
@@ -388,7 +393,7 @@ __device__ __forceinline__ void xy_issue_plane(const KParams &p, const double *_
         continue;
 #pragma unroll
       for (int f = 0; f < 5; ++f) cp_async16(d + f * FSZ, qp + f * FS + off);
-      cp_async16(d + XF_G22 * FSZ, gp + 2 * FS + off);
+      cp_async16(PB + Gm::PB_G22 + hy * PX + hx, gp + 2 * FS + off);
     }
 #pragma unroll 1
     for (int idx = tid; idx < XY_TY * H2; idx += nthr) {
@@ -412,7 +417,7 @@ __device__ __forceinline__ void xy_issue_plane(const KParams &p, const double *_
         continue;
 #pragma unroll
       for (int f = 0; f < 5; ++f) cp_async8(d + f * FSZ, qp + f * FS + off);
-      cp_async8(d + XF_G22 * FSZ, gp + 2 * FS + off);
+      cp_async8(PB + Gm::PB_G22 + hy * PX + hx, gp + 2 * FS + off);
     }
 #pragma unroll 1
     for (int idx = tid; idx < XY_TY * HX; idx += nthr) {
@@ -512,7 +517,10 @@ __global__ void __launch_bounds__(XY_CTA, 1)
     xypass_kernel(const KParams p, const double *__restrict__ q, double *__restrict__ qout,
                   double *__restrict__ w, const double *__restrict__ gz,
                   double *__restrict__ rout,
-                  unsigned int *__restrict__ flag, const PlaneRange zr) {
+                  unsigned int *__restrict__ flag, const PlaneRange zr,
+                  const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tg22,
+                  const __grid_constant__ CUtensorMap tg02, const __grid_constant__ CUtensorMap tg12,
+                  const int use_tma) {
   // XF bits: 1 = two-register epilogue, 2 = symmetry in x/y, 4 = equation variants
   // (mu(T), conservative viscous work), which take symmetry at run time;
   // 8 = fused diagnostics (stage 1 of osbli_step_diag)
@@ -528,7 +536,7 @@ __global__ void __launch_bounds__(XY_CTA, 1)
   using Gm = XYGeom<M>;
   constexpr int HX = Gm::HX, HY = Gm::HY, PX = Gm::PX, FSZ = Gm::FSZ, NPT = Gm::NPT, TP = Gm::TP;
   constexpr int XO = Gm::XO, XC = Gm::XC;  // staged column offsets (odd m)
-  extern __shared__ double SM[];
+  extern __shared__ __align__(128) double SM[];
   double *PR = SM + Gm::OFF_PR;
   double *E0 = SM + Gm::OFF_E0, *E1 = SM + Gm::OFF_E1;
   double *XA = SM + Gm::OFF_XA, *XB = SM + Gm::OFF_XB;
@@ -565,6 +573,19 @@ __global__ void __launch_bounds__(XY_CTA, 1)
     // bytes at a time everywhere: a mirrored pair is reversed in memory, and pairs
     // on its interior tiles only measured slower (1.63 vs 1.55 ms at 256^3 o12)
     const bool pairs = !SYM && (p.nx % 2) == 0;
+    // TMA for tiles whose staged region lies inside the grid (no wrap): one 5-field box
+    // of Q and one box each of g22, g02, g12 per plane, completing on the plane
+    // buffer's mbarrier; the other tiles (and symmetric, debug builds) use cp.async
+    const bool tma = use_tma && pairs && !OSBLI_DEBUG_CHECKS && x0 - Gm::XC >= 0 &&
+                     x0 - Gm::XC + PX <= p.nx && y0 - M >= 0 && y0 + XY_TY + M <= p.ny;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(SM + Gm::OFF_BAR);
+    if (tma && lane == 0) {
+      mbar_init(bars, 1);
+      mbar_init(bars + 1, 1);
+    }
+    nbar_sync(7, XY_PROD);  // the mbarriers are initialised
+    constexpr unsigned TMA_BYTES =
+        (unsigned)((6 * FSZ + XY_TY * PX + HY * Gm::GP) * sizeof(double));
     for (int i = 0; i < nplanes; ++i) {
       const int b = i & 1;
       if (i >= 2) nbar_sync(4 + b, XY_CTA);
@@ -572,11 +593,24 @@ __global__ void __launch_bounds__(XY_CTA, 1)
         for (int k = lane; k < Gm::PBSZ; k += XY_PROD) SM[b * Gm::PBSZ + k] = dbg_nan();
         nbar_sync(7, XY_PROD);
       }
-      if (!OSBLI_XY_EXP_NOSTAGE || i < 2)  // experiment: staging cost upper bound (wrong results)
-        xy_issue_plane<M>(p, q, gz, SM + b * Gm::PBSZ, zs + i, cx, ry, lane, XY_PROD, pairs);
+      double *PB = SM + b * Gm::PBSZ;
+      if (tma) {
+        if (lane == 0) {
+          const int z = zs + i;
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+          mbar_expect_tx(bars + b, TMA_BYTES);
+          tma_load_box(PB, &tmq, x0 - Gm::XC, y0 - M, 0, z + p.G, bars + b);
+          tma_load_box(PB + Gm::PB_G22, &tg22, x0 - Gm::XC, y0 - M, 2, z, bars + b);
+          tma_load_box(PB + Gm::PB_G02, &tg02, x0 - Gm::XC, y0, 0, z, bars + b);
+          tma_load_box(PB + Gm::PB_G12, &tg12, x0, y0 - M, 1, z, bars + b);
+        }
+      } else if (!OSBLI_XY_EXP_NOSTAGE || i < 2) {  // experiment: staging cost bound (wrong results)
+        xy_issue_plane<M>(p, q, gz, PB, zs + i, cx, ry, lane, XY_PROD, pairs);
+      }
       xy_prefetch_epilogue(p, TR ? qout + qplane(p, 0) : w, zs + i, x0, y0, lane, XY_PROD);
       if (TR && p.read_w) xy_prefetch_epilogue(p, w, zs + i, x0, y0, lane, XY_PROD);
-      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      if (tma) mbar_wait(bars + b, (i >> 1) & 1);
+      else asm volatile("cp.async.wait_group 0;\n" ::: "memory");
       if (SYM && (p.sym[0] | p.sym[1])) {
         nbar_sync(7, XY_PROD);  // every producer's copies have landed
         xy_mirror_signs<M>(p, SM + b * Gm::PBSZ, x0, y0, lane, XY_PROD);
@@ -720,7 +754,7 @@ OSBLI_UNROLL(OSBLI_XY_FORM_UNROLL)
             const double g20 = XA[4 * NPT + pt];
             const double g01 = o.g[0][j], g11 = o.g[1][j], g21 = o.g[2][j];
             const double g02 = G02[ty * PX + col + XC], g12 = G12[(ty + M) * Gm::GP + col],
-                         g22 = S[XF_G22 * FSZ + c];
+                         g22 = S[Gm::PB_G22 + c];
             const double T = o.Tc[j];
             const double mu = p.visc ? sutherland_mu(p, T) : 1.0;
             const double dmu = p.visc ? sutherland_dmu(p, T, mu) : 0.0;
@@ -782,7 +816,7 @@ OSBLI_UNROLL(OSBLI_XY_FORM_UNROLL)
           const double g20 = XA[4 * NPT + pt];
           const double g01 = o.g[0][j], g11 = o.g[1][j], g21 = o.g[2][j];
           const double g02 = G02[ty * PX + col + XC], g12 = G12[(ty + M) * Gm::GP + col],
-                       g22 = S[XF_G22 * FSZ + c];
+                       g22 = S[Gm::PB_G22 + c];
           // y-parts of V_i: V0 += nu (D11 u0 + 1/3 D1 g10);
           // V1 += nu (4/3 D11 u1 + 1/3 (D1 g00 + D1 g22)); V2 += nu (D11 u2 + 1/3 D1 g12)
           const double V0y = p.nu * (o.d2u[0][j] + third * o.mixD[j]);
@@ -841,7 +875,7 @@ OSBLI_UNROLL(OSBLI_XY_FORM_UNROLL)
           // nu/3 D_x g02 (momentum z), and their work u_i V_i (D-7)
           constexpr int W = Gm::W;
           double v[W], ma[4];
-          ldwin<W, Gm::XW>(S + XF_G22 * FSZ + base, 1, v);
+          ldwin<W, Gm::XW>(S + Gm::PB_G22 + base, 1, v);
 #pragma unroll
           for (int j = 0; j < 4; ++j) ma[j] = (p.nu * third) * wd1<M, W>(p, v, j);
           ldwin<W, Gm::XW>(S + Gm::PB_G02 + row * PX + seg * XY_RX + XO, 1, v);
@@ -884,7 +918,7 @@ OSBLI_UNROLL(OSBLI_XY_FORM_UNROLL)
           // nu/3 D_y g12 (momentum z), and their work u_i V_i (D-7)
           constexpr int W = Gm::W;
           double v[W], ma[4];
-          ldwin<W>(S + XF_G22 * FSZ + base, PX, v);
+          ldwin<W>(S + Gm::PB_G22 + base, PX, v);
 #pragma unroll
           for (int j = 0; j < 4; ++j) ma[j] = (p.nu * third) * wd1<M, W>(p, v, j);
           ldwin<W>(S + Gm::PB_G12 + (seg * XY_RY) * Gm::GP + col, Gm::GP, v);

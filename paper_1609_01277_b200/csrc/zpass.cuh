@@ -52,37 +52,6 @@ struct ZGeom {
 };
 static_assert((ZP_NF * 32) % 16 == 0, "the raw staging buffer must stay 128-byte aligned");
 
-// TMA: bulk tensor copy of one box of the Q buffer (tensor map over [planes][5][ny][nx])
-// into shared memory, completing on an mbarrier
-__device__ __forceinline__ void tma_load_plane(double *dst, const CUtensorMap *tm, int x, int y,
-                                               int zplane, uint64_t *bar) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
-  asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::"r"(d),
-      "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(0), "r"(zplane), "r"(b)
-      : "memory");
-}
-__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
-  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(b), "r"(count) : "memory");
-  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
-  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(b), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
-  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
-  asm volatile(
-      "{\n .reg .pred P;\n WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
-      " @!P bra WAIT_%=;\n}\n" ::"r"(b), "r"(parity)
-      : "memory");
-}
-
 template <int M>
 constexpr int zp_smem_bytes() {
   return ZGeom<M>::BYTES;
@@ -256,7 +225,7 @@ __global__ void __launch_bounds__(ZP_THREADS, OSBLI_ZP_MINB)
         const int j = warp * PW + lane;
         int fl_;
         const int zb_ = zread_t<SYMZ>(p, zs + kk * ZP_TZ + M + j, fl_) + p.G;
-        tma_load_plane(RB + j * 5 * 32, &tmq, x0, y, zb_, tbar);
+        tma_load_box(RB + j * 5 * 32, &tmq, x0, y, 0, zb_, tbar);
       }
       return;
     }

@@ -1,5 +1,4 @@
-timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_gpu_production.py -x -q -m gpu > gpurun_out/t_tma.log 2>&1; echo rc=$? >> gpurun_out/t_tma.log
-for rep in 1 2; do for o in 4 8 12; do
-  python tools/quickbench.py 256 $o 30 2>&1 | tail -n 1
-  OSBLI_ZP_TMA=0 python tools/quickbench.py 256 $o 30 2>&1 | tail -n 1
-done; done > gpurun_out/ab_tma2.txt 2>&1
+timeout 1500 python -m pytest tests -x -q -m gpu > gpurun_out/t_xtma_all.log 2>&1; echo rc=$? >> gpurun_out/t_xtma_all.log
+OSBLI_NO_SPLIT=1 timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_slabs.py tests/test_gpu_combinations.py -x -q -m gpu > gpurun_out/t_xtma_ns.log 2>&1; echo rc=$? >> gpurun_out/t_xtma_ns.log
+timeout 300 python bench.py > gpurun_out/r2g_bench.json 2> gpurun_out/r2g_bench.err
+timeout 300 python bench.py --no-cpu-baseline --config tgv256_o8 > gpurun_out/r2g_bench_o8.json 2>> gpurun_out/r2g_bench.err
