@@ -102,13 +102,7 @@ def run_scalar(args, cfg):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(torch.cuda.current_device()) as clk:
         # warm-up of at least W steps and 1 s (the clock sampler's start-up)
-        t_w = time.perf_counter()
-        while True:
-            for _ in range(args.warmup):
-                s.step(1)
-            s.sync()
-            if time.perf_counter() - t_w > 1.0:
-                break
+        warm_up(lambda: s.step(1), s.sync, args.warmup, world)
         if world > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize()
@@ -143,6 +137,26 @@ def run_scalar(args, cfg):
         "clocks": clk.summary(),
         "gpu_launches": 3 * args.steps,
     }), flush=True)
+
+
+def warm_up(step, sync, warmup, world, min_s=1.0):
+    """Rounds of `warmup` steps until at least min_s seconds have passed on every
+    rank; the decision is collective (a MIN all-reduce), so all ranks take the same
+    number of steps."""
+    import torch
+    t_w = time.perf_counter()
+    while True:
+        for _ in range(warmup):
+            step()
+        sync()
+        done = time.perf_counter() - t_w > min_s
+        if world > 1:
+            dev = "cuda" if torch.cuda.is_available() else "cpu"  # nccl / gloo
+            t = torch.tensor([1.0 if done else 0.0], device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MIN)
+            done = bool(t.item() > 0.5)
+        if done:
+            return
 
 
 def measured_peaks():
@@ -363,14 +377,9 @@ def main():
 
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(torch.cuda.current_device()) as clk:
-        # warm-up (also covers nvidia-smi start-up so that samples land in the timed region)
-        t_w = time.perf_counter()
-        while True:
-            for _ in range(args.warmup):
-                solver.step(1)
-            solver.sync()
-            if time.perf_counter() - t_w > 1.0:
-                break
+        # warm-up (also covers nvidia-smi start-up so that samples land in the timed region);
+        # every rank takes the same number of steps (each step exchanges ghost planes)
+        warm_up(lambda: solver.step(1), solver.sync, args.warmup, world)
         # ---- timed region: K steps, device-timed with CUDA events on the solver stream
         launches0 = solver.kernel_launches
         solver.set_kernel_timing(True)
