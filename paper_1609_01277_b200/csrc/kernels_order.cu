@@ -341,12 +341,12 @@ inline bool no_split() {
 
 // TMA tensor maps of the solver's buffers, as 4-D fp64 tensors (x, y, field, plane):
 // Q buffers [nz + 2G][5][ny][nx] and Gz [nz][3][ny][nx].  Built once per (buffer,
-// shape, box) (a small cache); nullptr when TMA does not apply (odd nx: row strides
-// must be multiples of 16 bytes) or the driver entry point is missing, and the
-// kernels then stage with cp.async.
-const CUtensorMap *tensor_map(const double *ptr, int nx, int ny, int nf, int planes, int bx,
-                              int by, int bf) {
-  if (nx % 2 != 0) return nullptr;
+// shape, box) (a small cache) and copied out under the lock; false when TMA does not
+// apply (odd nx: row strides must be multiples of 16 bytes) or the driver entry point
+// is missing, and the kernels then stage with cp.async.
+bool tensor_map(const double *ptr, int nx, int ny, int nf, int planes, int bx, int by, int bf,
+                CUtensorMap *out) {
+  if (nx % 2 != 0) return false;
   static std::mutex mu;
   static PFN_cuTensorMapEncodeTiled encode = nullptr;
   static bool tried = false;
@@ -367,10 +367,13 @@ const CUtensorMap *tensor_map(const double *ptr, int nx, int ny, int nf, int pla
         qr == cudaDriverEntryPointSuccess)
       encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
   }
-  if (!encode) return nullptr;
+  if (!encode) return false;
   const int key[7] = {nx, ny, nf, planes, bx, by, bf};
   for (const Entry &e : cache)
-    if (e.ptr == ptr && std::memcmp(e.key, key, sizeof(key)) == 0) return &e.map;
+    if (e.ptr == ptr && std::memcmp(e.key, key, sizeof(key)) == 0) {
+      *out = e.map;
+      return true;
+    }
   Entry &e = cache[next];
   next = (next + 1) % 32;
   const cuuint64_t dims[4] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)nf, (cuuint64_t)planes};
@@ -382,17 +385,18 @@ const CUtensorMap *tensor_map(const double *ptr, int nx, int ny, int nf, int pla
              box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
     e.ptr = nullptr;
-    return nullptr;
+    return false;
   }
   e.ptr = ptr;
   std::memcpy(e.key, key, sizeof(key));
-  return &e.map;
+  *out = e.map;
+  return true;
 }
 
 // z-pass staging box: one plane of a 32-column pencil, all five fields
-const CUtensorMap *qbuf_tensor_map(const double *q, const KParams &p) {
-  if (p.nx < ZP_TX) return nullptr;
-  return tensor_map(q, p.nx, p.ny, 5, p.nz + 2 * p.G, ZP_TX, 1, 5);
+bool qbuf_tensor_map(const double *q, const KParams &p, CUtensorMap *out) {
+  if (p.nx < ZP_TX) return false;
+  return tensor_map(q, p.nx, p.ny, 5, p.nz + 2 * p.G, ZP_TX, 1, 5, out);
 }
 
 // OSBLI_ZP_TMA=0 / OSBLI_XY_TMA=0 (testing): stage the z-pass / xy-pass with cp.async everywhere
@@ -435,10 +439,10 @@ cudaError_t zpass_launch(const KParams &p, const double *q, double *w, double *g
     if (g > 0 && g < gx * gy) grid.x = g;
   }
 #endif
-  const CUtensorMap *tm = zp_tma_enabled() ? qbuf_tensor_map(q, p) : nullptr;
-  CUtensorMap none;
-  std::memset(&none, 0, sizeof(none));
-  kern<<<grid, ZP_THREADS, smem, s>>>(p, q, w, gz, zr, tm ? *tm : none, tm ? 1 : 0);
+  CUtensorMap tm;
+  std::memset(&tm, 0, sizeof(tm));
+  const bool tma = zp_tma_enabled() && qbuf_tensor_map(q, p, &tm);
+  kern<<<grid, ZP_THREADS, smem, s>>>(p, q, w, gz, zr, tm, tma ? 1 : 0);
   return cudaGetLastError();
 }
 
@@ -475,18 +479,17 @@ cudaError_t xypass_launch(const KParams &p, const double *q, double *qout, doubl
   const PlaneRange zr = plane_range(zb, ze, zb1, ze1, seg, &ntot);
   dim3 grid((p.nx + ws::XY_TX - 1) / ws::XY_TX, (p.ny + ws::XY_TY - 1) / ws::XY_TY, ntot);
   using Gm = ws::XYGeom<M>;
-  const CUtensorMap *tq = nullptr, *t22 = nullptr, *t02 = nullptr, *t12 = nullptr;
-  if (xy_tma_enabled() && p.nx >= Gm::PX && p.ny >= Gm::HY) {
-    tq = tensor_map(q, p.nx, p.ny, 5, p.nz + 2 * p.G, Gm::PX, Gm::HY, 5);
-    t22 = tensor_map(gz, p.nx, p.ny, 3, p.nz, Gm::PX, Gm::HY, 1);
-    t02 = tensor_map(gz, p.nx, p.ny, 3, p.nz, Gm::PX, ws::XY_TY, 1);
-    t12 = tensor_map(gz, p.nx, p.ny, 3, p.nz, Gm::GP, Gm::HY, 1);
-  }
-  const bool tma = tq && t22 && t02 && t12;
-  CUtensorMap none;
-  std::memset(&none, 0, sizeof(none));
-  kern<<<grid, ws::XY_CTA, smem, s>>>(p, q, qout, w, gz, rout, flag, zr, tma ? *tq : none,
-                                      tma ? *t22 : none, tma ? *t02 : none, tma ? *t12 : none,
+  CUtensorMap tq, t22, t02, t12;
+  std::memset(&tq, 0, sizeof(tq));
+  std::memset(&t22, 0, sizeof(t22));
+  std::memset(&t02, 0, sizeof(t02));
+  std::memset(&t12, 0, sizeof(t12));
+  const bool tma = xy_tma_enabled() && p.nx >= Gm::PX && p.ny >= Gm::HY &&
+                   tensor_map(q, p.nx, p.ny, 5, p.nz + 2 * p.G, Gm::PX, Gm::HY, 5, &tq) &&
+                   tensor_map(gz, p.nx, p.ny, 3, p.nz, Gm::PX, Gm::HY, 1, &t22) &&
+                   tensor_map(gz, p.nx, p.ny, 3, p.nz, Gm::PX, ws::XY_TY, 1, &t02) &&
+                   tensor_map(gz, p.nx, p.ny, 3, p.nz, Gm::GP, Gm::HY, 1, &t12);
+  kern<<<grid, ws::XY_CTA, smem, s>>>(p, q, qout, w, gz, rout, flag, zr, tq, t22, t02, t12,
                                       tma ? 1 : 0);
   return cudaGetLastError();
 }
