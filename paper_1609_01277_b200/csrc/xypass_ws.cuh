@@ -73,10 +73,11 @@ __device__ __forceinline__ void nbar_arrive(int id, int count) {
 #define OSBLI_XY_MIXX_B 1
 #endif
 constexpr bool XY_MIXX_B = OSBLI_XY_MIXX_B != 0;
+// OSBLI_XY_MIXY_B: bit 0 = nu/3 D_y g22 (momentum y), bit 1 = nu/3 D_y g12 (momentum z)
 #ifndef OSBLI_XY_MIXY_B
 #define OSBLI_XY_MIXY_B 0
 #endif
-constexpr bool XY_MIXY_B = OSBLI_XY_MIXY_B != 0;
+constexpr int XY_MIXY_B = OSBLI_XY_MIXY_B;
 // z-planes per CTA: 16 at orders 2 and 4 (the pipeline fill of a segment weighs
 // more against the short stencils: -3 % xy-pass at o4), 8 above (neutral at 16)
 #ifndef OSBLI_XY_SEG
@@ -223,7 +224,8 @@ struct VelResult {
 
 // TW: also the temperature stencils (heat flux, and D_d T, T for the variants);
 // without them the heat flux is group B's (conservative_dir<.., HEAT = true>)
-template <int M, int DIR, bool TW, bool NOMIX = false>
+// NOMIX: bit 0 skips D_d g22 (mixA), bit 1 the second mixed stencil (mixB)
+template <int M, int DIR, bool TW, int NOMIX = 0>
 __device__ __forceinline__ void velocity_dir(const KParams &p, const double *S, const double *PR,
                                              int base, int st, const double *gmix, int gst,
                                              const double *E0, const double *E1, int ebase,
@@ -256,10 +258,12 @@ __device__ __forceinline__ void velocity_dir(const KParams &p, const double *S, 
       o.Tc[j] = v[j + M];
     }
   }
-  if (!NOMIX) {
+  if (!(NOMIX & 1)) {
     ldwin<W, PW>(S + Gm::PB_G22 + base, st, v);  // D_d g22
 #pragma unroll
     for (int j = 0; j < 4; ++j) o.mixA[j] = wd1<M, W>(p, v, j);
+  }
+  if (!(NOMIX & 2)) {
     ldwin<W, PW>(gmix, gst, v);  // DIR 0: D_x g02 = D_z g00 ; DIR 1: D_y g12 = D_z g11
 #pragma unroll
     for (int j = 0; j < 4; ++j) o.mixB[j] = wd1<M, W>(p, v, j);
@@ -665,7 +669,7 @@ OSBLI_UNROLL(OSBLI_XY_FORM_UNROLL)
         const int base = hy * PX + seg * XY_RX + XO;  // window start (staged coords)
         const int pt0 = row * TP + seg * XY_RX;
         VelResult<M> o;
-        velocity_dir<M, 0, VAR, MIXB>(
+        velocity_dir<M, 0, VAR, MIXB ? 3 : 0>(
             p, S, PR, base, 1, G02 + row * PX + seg * XY_RX + XO, 1, E0, E1, 0, o);
         // B has finished reading XA (its epilogue of the previous plane)
         if (i > 0) nbar_sync(10, XY_THREADS);
@@ -745,7 +749,7 @@ OSBLI_UNROLL(OSBLI_XY_FORM_UNROLL)
           }
         }
         VelResult<M> o;
-        velocity_dir<M, 1, VAR, !VAR && XY_MIXY_B>(p, S, PR, base, PX, G12 + gbase, Gm::GP, E0,
+        velocity_dir<M, 1, VAR, VAR ? 0 : XY_MIXY_B>(p, S, PR, base, PX, G12 + gbase, Gm::GP, E0,
                                                           E1, ebase, o);
         double dg[3] = {0.0, 0.0, 0.0};  // fused diagnostics sums of this thread's points (DIAG)
         if (VAR) {
@@ -824,10 +828,10 @@ OSBLI_UNROLL(OSBLI_XY_FORM_UNROLL)
           // y-parts of V_i: V0 += nu (D11 u0 + 1/3 D1 g10);
           // V1 += nu (4/3 D11 u1 + 1/3 (D1 g00 + D1 g22)); V2 += nu (D11 u2 + 1/3 D1 g12)
           const double V0y = p.nu * (o.d2u[0][j] + third * o.mixD[j]);
-          // (XY_MIXY_B: the 1/3 D1 g22 and 1/3 D1 g12 parts are group B's)
+          // (XY_MIXY_B bits: the 1/3 D1 g22 and 1/3 D1 g12 parts are group B's)
           const double V1y = p.nu * (o.d2u[1][j] + third * (o.d2u[1][j] + o.mixC[j] +
-                                                            (XY_MIXY_B ? 0.0 : o.mixA[j])));
-          const double V2y = p.nu * (o.d2u[2][j] + (XY_MIXY_B ? 0.0 : third * o.mixB[j]));
+                                                            ((XY_MIXY_B & 1) ? 0.0 : o.mixA[j])));
+          const double V2y = p.nu * (o.d2u[2][j] + ((XY_MIXY_B & 2) ? 0.0 : third * o.mixB[j]));
           const double V0 = XA[0 * NPT + pt] + V0y, V1 = XA[1 * NPT + pt] + V1y,
                        V2 = XA[2 * NPT + pt] + V2y;
           const double thxy = g00 + g11, th = thxy + g22;
@@ -918,23 +922,34 @@ OSBLI_UNROLL(OSBLI_XY_FORM_UNROLL)
         double R[5][4];
         conservative_dir<M, 1, !VAR>(p, S, PR, base, PX, R);
         if (!VAR && XY_MIXY_B) {
-          // the y mixed-derivative viscous parts, nu/3 D_y g22 (momentum y) and
+          // the y mixed-derivative viscous parts, nu/3 D_y g22 (momentum y) and/or
           // nu/3 D_y g12 (momentum z), and their work u_i V_i (D-7)
           constexpr int W = Gm::W;
-          double v[W], ma[4];
-          ldwin<W>(S + Gm::PB_G22 + base, PX, v);
+          double v[W], ma[4] = {0.0, 0.0, 0.0, 0.0}, mb[4] = {0.0, 0.0, 0.0, 0.0};
+          if (XY_MIXY_B & 1) {
+            ldwin<W>(S + Gm::PB_G22 + base, PX, v);
 #pragma unroll
-          for (int j = 0; j < 4; ++j) ma[j] = (p.nu * third) * wd1<M, W>(p, v, j);
-          ldwin<W>(S + Gm::PB_G12 + (seg * XY_RY) * Gm::GP + col, Gm::GP, v);
+            for (int j = 0; j < 4; ++j) ma[j] = (p.nu * third) * wd1<M, W>(p, v, j);
+          }
+          if (XY_MIXY_B & 2) {
+            ldwin<W>(S + Gm::PB_G12 + (seg * XY_RY) * Gm::GP + col, Gm::GP, v);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) mb[j] = (p.nu * third) * wd1<M, W>(p, v, j);
+          }
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            const double mb = (p.nu * third) * wd1<M, W>(p, v, j);
             const int c = base + (M + j) * PX;
             const double r = PR[XP_R * FSZ + c];
-            const double u1 = __dmul_rn(S[XF_M1 * FSZ + c], r), u2 = __dmul_rn(S[XF_M2 * FSZ + c], r);
-            R[2][j] += ma[j];
-            R[3][j] += mb;
-            R[4][j] = fma(u1, ma[j], fma(u2, mb, R[4][j]));
+            if (XY_MIXY_B & 1) {
+              const double u1 = __dmul_rn(S[XF_M1 * FSZ + c], r);
+              R[2][j] += ma[j];
+              R[4][j] = fma(u1, ma[j], R[4][j]);
+            }
+            if (XY_MIXY_B & 2) {
+              const double u2 = __dmul_rn(S[XF_M2 * FSZ + c], r);
+              R[3][j] += mb[j];
+              R[4][j] = fma(u2, mb[j], R[4][j]);
+            }
           }
         }
         if (i + 1 < nplanes) nbar_arrive(9, XY_THREADS);  // done with PR: A may refill it
