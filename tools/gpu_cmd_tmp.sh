@@ -1,1 +1,1 @@
-timeout 900 python -m pytest tests/test_gpu_tma.py -x -q -m gpu > gpurun_out/t_tmatest.log 2>&1; echo rc=$? >> gpurun_out/t_tmatest.log
+REPS=3 STEPS=30 bash tools/ab_run.sh ab_wpf.txt "4 8 12" cur nopf
