@@ -585,27 +585,6 @@ int run_stage(osbli_ctx *h, int s, bool exchange = true, bool divh = true) {
     h->ev_used += 3;
   }
   if (!h->slab) {
-    static const bool exp_conc = [] { const char *e = std::getenv("OSBLI_EXP_CONC"); return e && e[0] == '1'; }();
-    if (exp_conc) {
-      // experiment only (results wrong): the z-pass on a side stream concurrently
-      // with the xy-pass, to measure what overlapping the two kernels could buy
-      static cudaStream_t xs = nullptr;
-      static cudaEvent_t e0 = nullptr, e1 = nullptr;
-      if (!xs) {
-        cudaStreamCreateWithFlags(&xs, cudaStreamNonBlocking);
-        cudaEventCreateWithFlags(&e0, cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&e1, cudaEventDisableTiming);
-      }
-      CK(h, cudaEventRecord(e0, h->stream));
-      CK(h, cudaStreamWaitEvent(xs, e0, 0));
-      CK(h, osbli::launch_zpass(p, qin, wz, h->b.gz, 0, h->nz, xs, &h->launches));
-      CK(h, osbli::launch_xypass(p, qin, qout, h->b.w, h->b.gz, nullptr, h->b.flag, 0, h->nz,
-                                 h->stream, &h->launches));
-      CK(h, cudaEventRecord(e1, xs));
-      CK(h, cudaStreamWaitEvent(h->stream, e1, 0));
-      h->cur ^= 1;
-      return OSBLI_OK;
-    }
     if (ev) CK(h, cudaEventRecord(ev[0], h->stream));
     CK(h, osbli::launch_zpass(p, qin, wz, h->b.gz, 0, h->nz, h->stream, &h->launches));
     if (ev) CK(h, cudaEventRecord(ev[1], h->stream));
