@@ -78,11 +78,12 @@ constexpr bool XY_MIXX_B = OSBLI_XY_MIXX_B != 0;
 #define OSBLI_XY_MIXY_B 0
 #endif
 constexpr int XY_MIXY_B = OSBLI_XY_MIXY_B;
-// z-planes per CTA: 16 at orders 2 and 4 (the pipeline fill of a segment weighs
-// more against the short stencils: -3 % xy-pass at o4), 8 above (neutral at 16)
+// z-planes per CTA: 16 at orders 2, 4 (the pipeline fill of a segment weighs more
+// against the short stencils: -3 % xy-pass at o4) and 12 (-0.5 %), 8 at 6-10 (16
+// is +0.3 % at o8)
 #ifndef OSBLI_XY_SEG
 template <int M>
-constexpr int xy_seg() { return M <= 2 ? 16 : 8; }
+constexpr int xy_seg() { return (M <= 2 || M >= 6) ? 16 : 8; }
 #else
 template <int M>
 constexpr int xy_seg() { return OSBLI_XY_SEG; }
