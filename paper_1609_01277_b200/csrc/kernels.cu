@@ -25,10 +25,71 @@
 // dense contraction).  Periodic wrap in x and y is done in-kernel; in
 // z either in-kernel (one GPU) or through ghost planes (slab decomposition).
 // =============================================================================
+#include <cudaTypedefs.h>
+
+#include <cstring>
+#include <mutex>
+
 #include "device_common.cuh"
 #include "dispatch.h"
 
 namespace osbli {
+
+// TMA tensor maps of the solver's buffers, as 4-D fp64 tensors (x, y, field, plane):
+// Q buffers [nz + 2G][5][ny][nx] and Gz [nz][3][ny][nx].  Built once per (buffer,
+// shape, box) (a small cache) and copied out under the lock; false when TMA does not
+// apply (odd nx: row strides must be multiples of 16 bytes) or the driver entry point
+// is missing, and the kernels then stage with cp.async.
+bool tensor_map(const double *ptr, int nx, int ny, int nf, int planes, int bx, int by, int bf,
+                CUtensorMap *out) {
+  if (nx % 2 != 0) return false;
+  static std::mutex mu;
+  static PFN_cuTensorMapEncodeTiled encode = nullptr;
+  static bool tried = false;
+  struct Entry {
+    const double *ptr;
+    int key[7];
+    CUtensorMap map;
+  };
+  static Entry cache[32];
+  static int next = 0;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!tried) {
+    tried = true;
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr) ==
+            cudaSuccess &&
+        qr == cudaDriverEntryPointSuccess)
+      encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
+  }
+  if (!encode) return false;
+  const int key[7] = {nx, ny, nf, planes, bx, by, bf};
+  for (const Entry &e : cache)
+    if (e.ptr == ptr && std::memcmp(e.key, key, sizeof(key)) == 0) {
+      *out = e.map;
+      return true;
+    }
+  Entry &e = cache[next];
+  next = (next + 1) % 32;
+  const cuuint64_t dims[4] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)nf, (cuuint64_t)planes};
+  const cuuint64_t strides[3] = {(cuuint64_t)nx * 8, (cuuint64_t)nx * ny * 8,
+                                 (cuuint64_t)nf * nx * ny * 8};
+  const cuuint32_t box[4] = {(cuuint32_t)bx, (cuuint32_t)by, (cuuint32_t)bf, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  if (encode(&e.map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double *>(ptr), dims, strides,
+             box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+    e.ptr = nullptr;
+    return false;
+  }
+  e.ptr = ptr;
+  std::memcpy(e.key, key, sizeof(key));
+  *out = e.map;
+  return true;
+}
+
+
 namespace {
 // per-plane partials [nz][3] = the plane's tile partials summed in tile order
 __global__ void diag_tiles_kernel(const double *__restrict__ tpart, int nz, int ntiles,

@@ -1,6 +1,7 @@
 // Internal interface between the C-ABI runtime (api.cpp) and the sm_100a
 // kernels (kernels.cu).  Not part of the public ABI.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace osbli {
@@ -109,5 +110,12 @@ cudaError_t launch_abi_to_internal(const KParams &p, const double *src, double *
                                    long long *launches);
 cudaError_t launch_internal_to_abi(const KParams &p, const double *q, double *dst, int nfields,
                                    int ghosted, cudaStream_t s, long long *launches);
+
+// TMA tensor map of a device buffer viewed as a 4-D fp64 tensor (x: nx, y: ny,
+// field: nf, plane: planes; x fastest) with a (bx, by, bf, 1) box (kernels.cu).
+// Cached per (buffer, shape, box); false when TMA does not apply (odd nx) or the
+// driver entry point is missing.
+bool tensor_map(const double *ptr, int nx, int ny, int nf, int planes, int bx, int by, int bf,
+                CUtensorMap *out);
 
 }  // namespace osbli
