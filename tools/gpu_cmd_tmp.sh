@@ -1,2 +1,4 @@
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_production.py tests/test_gpu_tma.py -x -q -m gpu > gpurun_out/t_qsp.log 2>&1; echo rc=$? >> gpurun_out/t_qsp.log
-REPS=3 STEPS=30 bash tools/ab_run.sh ab_qsp2.txt "4 8 12" cur noqsp
+timeout 300 python bench.py > gpurun_out/r2z_bench_tgv256_o12.json 2> gpurun_out/r2z.err
+timeout 300 python bench.py --no-cpu-baseline --config tgv256_o8 > gpurun_out/r2z_bench_tgv256_o8.json 2>> gpurun_out/r2z.err
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/r2z_launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/r2z_ncu_launch.log 2>&1
+for o in 2 4 6 8 10 12; do python tools/quickbench.py 256 $o 30 2>&1 | tail -n 1; done > gpurun_out/r2z_orders.txt
