@@ -1,5 +1,7 @@
 """Experiment timing (no kernel timing events): n order steps -> ms/step.
-Used with OSBLI_EXP_CONC / OSBLI_ZP_GRID variant builds (results are wrong there)."""
+Used for the z/xy overlap measurement of DESIGN.md §5b with OSBLI_ZP_GRID (a
+persistent z-pass grid, -DOSBLI_ZP_PERSIST=1 builds) and the OSBLI_EXP_CONC switch
+of run_stage (commit 032e30c, removed since; results were wrong by design)."""
 import math
 import os
 import sys
