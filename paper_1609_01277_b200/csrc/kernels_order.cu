@@ -192,67 +192,76 @@ __global__ void __launch_bounds__(256, 2) diag_kernel(const KParams p, const dou
 // direction j) added to the energy of the finished stage (D-27):
 //   residual: R_E += D;  2N: W_E += dt D (write_w), Q'_E += B dt D;
 //   two-register: Q'_E += alpha dt D, Q_old_E += beta dt D (write_w).
-// A CTA covers a 32 x 8 tile of the plane and marches through DH_Z planes:
-// per plane H_x (tile rows + x halo) and H_y (tile columns + y halo) are staged in
-// shared memory (the next plane's values are loaded into registers while the
-// current one is computed); H_z comes from a per-thread register window along z.
-constexpr int DH_Z = 8;
+// A CTA covers a 32 x 16 tile of the plane and marches through DH_Z = 16 planes,
+// one output per thread and plane.  Per plane H_x (tile rows + x halo) and H_y
+// (tile columns + y halo) are staged in shared memory, double-buffered: the next
+// plane's cp.async copies overlap the current one (one barrier per plane; the
+// mirrored halo values of symmetric boundaries are negated by their own copier
+// after landing).  H_z comes from a register window along z that slides by
+// renaming (fully unrolled plane loop, loads issued two planes ahead); the
+// read-modify-write operands are loaded a plane ahead.
+constexpr int DH_Z = 16, DH_TY = 16, DH_THREADS = 32 * DH_TY;
 template <int M>
 struct DHGeom {
-  static constexpr int XW = 32 + 2 * M;                       // H_x row width
-  static constexpr int NX = 8 * XW, NY = (8 + 2 * M) * 32;    // staged elements
-  static constexpr int PER = (NX + NY + 255) / 256;           // per thread
+  static constexpr int XW = 32 + 2 * M;                           // H_x row width
+  static constexpr int NX = DH_TY * XW, NY = (DH_TY + 2 * M) * 32;  // staged elements
+  static constexpr int N = NX + NY;
+  static constexpr int PER = (N + DH_THREADS - 1) / DH_THREADS;   // per thread
 };
 template <int M, bool SYM>
-__device__ __forceinline__ void divh_fetch(const KParams &p, const double *__restrict__ H, int z,
-                                           int x0, int y0, int tid, double (&v)[DHGeom<M>::PER]) {
+__global__ void __launch_bounds__(DH_THREADS, 2) divh_kernel(const KParams p,
+                                                             const double *__restrict__ H,
+                                                             double *__restrict__ qout,
+                                                             double *__restrict__ w,
+                                                             double *__restrict__ rout,
+                                                             unsigned int *__restrict__ flag,
+                                                             int zb, int ze) {
   using G = DHGeom<M>;
-  const size_t FS = (size_t)p.nx * p.ny;
-  const double *hp = H + (size_t)z * 3 * FS;
-#pragma unroll
-  for (int r = 0; r < G::PER; ++r) {
-    const int idx = tid + 256 * r;
-    v[r] = 0.0;
-    if (idx < G::NX) {  // H_x: row ty, column c of the x-extended row
-      const int ty = idx / G::XW, c = idx - ty * G::XW;
-      int f;
-      const int gx = bmap_t<SYM>(x0 - M + c, p.nx, p.sym[0], f);
-      const int gy = min(y0 + ty, p.ny - 1);
-      const double h = __ldg(hp + (size_t)gy * p.nx + gx);
-      v[r] = f ? -h : h;
-    } else if (idx < G::NX + G::NY) {  // H_y: row c of the y-extended tile, column tx
-      const int j = idx - G::NX, c = j >> 5, tx = j & 31;
-      int f;
-      const int gy = bmap_t<SYM>(y0 - M + c, p.ny, p.sym[1], f);
-      const int gx = min(x0 + tx, p.nx - 1);
-      const double h = __ldg(hp + FS + (size_t)gy * p.nx + gx);
-      v[r] = f ? -h : h;
-    }
-  }
-}
-
-template <int M, bool SYM>
-__global__ void __launch_bounds__(256, 4) divh_kernel(const KParams p,
-                                                      const double *__restrict__ H,
-                                                      double *__restrict__ qout,
-                                                      double *__restrict__ w,
-                                                      double *__restrict__ rout,
-                                                      unsigned int *__restrict__ flag, int zb,
-                                                      int ze) {
-  using G = DHGeom<M>;
-  __shared__ double sh[G::NX + G::NY];
+  __shared__ double sh[2][G::N];
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
-  const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 8;
+  const int x0 = blockIdx.x * 32, y0 = blockIdx.y * DH_TY;
   const int x = x0 + tx, y = y0 + ty;
   const bool valid = x < p.nx && y < p.ny;
   const int z0 = zb + blockIdx.z * DH_Z;
   const int nzo = min(DH_Z, ze - z0);
   const size_t FS = (size_t)p.nx * p.ny;
   const size_t off = (size_t)min(y, p.ny - 1) * p.nx + min(x, p.nx - 1);
-  // register window of H_z along z
-  double hz[DH_Z + 2 * M];
+  // in-plane offsets (component included) of the values this thread stages, and
+  // whether they come through an odd number of mirrors (H_j is odd in j)
+  int hoff[G::PER];
+  bool hneg[G::PER];
 #pragma unroll
-  for (int t = 0; t < DH_Z + 2 * M; ++t) {
+  for (int r = 0; r < G::PER; ++r) {
+    const int idx = tid + DH_THREADS * r;
+    hoff[r] = 0;
+    hneg[r] = false;
+    if (idx < G::NX) {  // H_x: row c of the tile, column cc of the x-extended row
+      const int c = idx / G::XW, cc = idx - c * G::XW;
+      int f;
+      const int gx = bmap_t<SYM>(x0 - M + cc, p.nx, p.sym[0], f);
+      hoff[r] = min(y0 + c, p.ny - 1) * p.nx + gx;
+      hneg[r] = f != 0;
+    } else if (idx < G::N) {  // H_y: row c of the y-extended tile, column cx
+      const int j = idx - G::NX, c = j >> 5, cx = j & 31;
+      int f;
+      const int gy = bmap_t<SYM>(y0 - M + c, p.ny, p.sym[1], f);
+      hoff[r] = (int)FS + gy * p.nx + min(x0 + cx, p.nx - 1);
+      hneg[r] = f != 0;
+    }
+  }
+  auto stage = [&](int j, int b) {  // plane z0 + j -> buffer b
+    const double *hp = H + (size_t)(z0 + j) * 3 * FS;
+#pragma unroll
+    for (int r = 0; r < G::PER; ++r) {
+      const int idx = tid + DH_THREADS * r;
+      if (idx < G::N) cp_async8(&sh[b][idx], hp + hoff[r]);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  // register window of H_z along z: hz[t] = H_z(z0 - m + t)
+  constexpr int HW = DH_Z + 2 * M, ZA = 2 * M + 2;
+  double hz[HW];
+  auto hzload = [&](int t) {
     hz[t] = 0.0;
     if (t < nzo + 2 * M) {
       int f;
@@ -260,50 +269,64 @@ __global__ void __launch_bounds__(256, 4) divh_kernel(const KParams p,
       const double v = __ldg(H + (size_t)zz * 3 * FS + 2 * FS + off);
       hz[t] = f ? -v : v;
     }
-  }
-  double nxt[G::PER];
-  divh_fetch<M, SYM>(p, H, z0, x0, y0, tid, nxt);
+  };
+#pragma unroll
+  for (int t = 0; t < (ZA < HW ? ZA : HW); ++t) hzload(t);
+  stage(0, 0);
+  // this plane's read-modify-write operands, loaded a plane ahead
+  const bool rmw = valid && !rout;
+  auto rmw_load = [&](int j, double &qo_, double &wo_) {
+    qo_ = 0.0;
+    wo_ = 0.0;
+    if (rmw && j < nzo) {
+      const int z = z0 + j;
+      qo_ = qout[qplane(p, z) + 4 * FS + off];
+      if (p.write_w) wo_ = w[(size_t)z * 5 * FS + 4 * FS + off];
+    }
+  };
+  double qn_old, wn_old;
+  rmw_load(0, qn_old, wn_old);
   bool bad = false;
 #pragma unroll
   for (int j = 0; j < DH_Z; ++j) {
-    if (j >= nzo) break;
-    const int z = z0 + j;
-    // this plane's read-modify-write operands, in flight during the staging below
-    const size_t o = (size_t)z * 5 * FS + 4 * FS + off;
-    double *qe = qout ? qout + qplane(p, z) + 4 * FS + off : nullptr;
-    double q_old = 0.0, w_old = 0.0;
-    if (valid && !rout) {
-      q_old = *qe;
-      if (p.write_w) w_old = w[o];
-    }
-    __syncthreads();  // the previous plane's reads are done
+    if (j < nzo) {
+      if (j + ZA < HW) hzload(j + ZA);
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      if (SYM) {  // mirrored halo values change sign (each copier fixes its own)
 #pragma unroll
-    for (int r = 0; r < G::PER; ++r) {
-      const int idx = tid + 256 * r;
-      if (idx < G::NX + G::NY) sh[idx] = nxt[r];
-    }
-    __syncthreads();
-    if (j + 1 < nzo) divh_fetch<M, SYM>(p, H, z + 1, x0, y0, tid, nxt);
-    const double *rx = sh + ty * G::XW + tx + M;
-    const double *cy = sh + G::NX + (ty + M) * 32 + tx;
-    double sx = 0.0, sy = 0.0, sz = 0.0;
+        for (int r = 0; r < G::PER; ++r) {
+          const int idx = tid + DH_THREADS * r;
+          if (idx < G::N && hneg[r]) sh[j & 1][idx] = -sh[j & 1][idx];
+        }
+      }
+      __syncthreads();  // plane j staged; every thread is done with plane j - 1's buffer
+      if (j + 1 < nzo) stage(j + 1, (j + 1) & 1);
+      const double q_old = qn_old, w_old = wn_old;
+      rmw_load(j + 1, qn_old, wn_old);
+      const double *rx = &sh[j & 1][ty * G::XW + tx + M];
+      const double *cy = &sh[j & 1][G::NX + (ty + M) * 32 + tx];
+      double sx = 0.0, sy = 0.0, sz = 0.0;
 #pragma unroll
-    for (int k = 1; k <= M; ++k) {
-      sx = fma(p.a[k - 1], rx[k] - rx[-k], sx);
-      sy = fma(p.a[k - 1], cy[32 * k] - cy[-32 * k], sy);
-      sz = fma(p.a[k - 1], hz[j + M + k] - hz[j + M - k], sz);
+      for (int k = 1; k <= M; ++k) {
+        sx = fma(p.a[k - 1], rx[k] - rx[-k], sx);
+        sy = fma(p.a[k - 1], cy[32 * k] - cy[-32 * k], sy);
+        sz = fma(p.a[k - 1], hz[j + M + k] - hz[j + M - k], sz);
+      }
+      if (valid) {
+        const int z = z0 + j;
+        const size_t o = (size_t)z * 5 * FS + 4 * FS + off;
+        const double d = sx + sy + sz;
+        if (rout) {
+          rout[o] += d;
+        } else {
+          const double dd = p.dt * d;
+          const double qn = fma(p.B, dd, q_old);
+          qout[qplane(p, z) + 4 * FS + off] = qn;
+          bad |= !isfinite(qn);
+          if (p.write_w) w[o] = fma(p.two_reg ? p.beta : 1.0, dd, w_old);
+        }
+      }
     }
-    if (!valid) continue;
-    const double d = sx + sy + sz;
-    if (rout) {
-      rout[o] += d;
-      continue;
-    }
-    const double dd = p.dt * d;
-    const double qn = fma(p.B, dd, q_old);
-    *qe = qn;
-    bad |= !isfinite(qn);
-    if (p.write_w) w[o] = fma(p.two_reg ? p.beta : 1.0, dd, w_old);
   }
   if (bad) atomicOr(flag, 1u);
 }
@@ -462,8 +485,8 @@ cudaError_t xypass_m<OSBLI_M>(const KParams &p, const double *q, double *qout, d
 template <>
 cudaError_t divh_m<OSBLI_M>(const KParams &p, double *q_out, double *w, double *r_out,
                             unsigned int *flag, int zb, int ze, cudaStream_t s) {
-  const dim3 grid((p.nx + 31) / 32, (p.ny + 7) / 8, (ze - zb + DH_Z - 1) / DH_Z);
-  const dim3 block(32, 8);
+  const dim3 grid((p.nx + 31) / 32, (p.ny + DH_TY - 1) / DH_TY, (ze - zb + DH_Z - 1) / DH_Z);
+  const dim3 block(32, DH_TY);
   if (p.sym[0] || p.sym[1])
     divh_kernel<OSBLI_M, true><<<grid, block, 0, s>>>(p, p.hflux, q_out, w, r_out, flag, zb, ze);
   else
