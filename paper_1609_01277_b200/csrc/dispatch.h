@@ -9,7 +9,7 @@
 namespace osbli {
 
 constexpr int DG_TY = 8;  // diagnostics tile rows (tile 32 x DG_TY)
-constexpr int DG_Z = 8;   // diagnostics planes per CTA
+constexpr int DG_Z = 16;  // diagnostics planes per CTA
 
 namespace detail {
 template <int M>

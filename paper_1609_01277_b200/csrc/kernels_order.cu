@@ -48,23 +48,27 @@ namespace {
 // Per-(plane, tile) partial sums of the integrands of the diagnostics (
 // D-11, D-12): 1/2 rho u_j u_j, 1/2 rho |omega|^2 and tau_ij du_i/dx_j, with the
 // velocity gradients g_ij = D_j u_i by the solver's first-derivative stencils.
-// A CTA covers a 32 x 8 tile of the plane and DG_Z consecutive planes: per plane
-// u_i on the tile rows with the x-halo (UX) and on the tile columns with the
-// y-halo (UY) are formed from rho, rho u_i in shared memory (u = m * (1/rho) as in
-// the stepping kernels, D-28); the z taps come from a per-thread register window
-// of u_i along z.  The 256 point values of each plane are reduced in a fixed
-// order (warp butterflies, then the 8 warps in order), so the partial of a
-// (plane, tile) depends on nothing but its data: diag_tiles_kernel then sums the
-// tiles of each plane in tile order, and the host sums the planes in global z
-// order, which makes the numbers independent of the slab decomposition.
+// A CTA covers a 32 x 8 tile of the plane and marches through DG_Z consecutive
+// planes: per plane rho, rho u_i on the tile rows with the x-halo (X part) and on
+// the tile columns with the y-halo (Y part) are staged in shared memory by cp.async,
+// double-buffered (the next plane's copies overlap the current one); once they
+// land, each copier turns its own values into u_i = m_i * (1/rho) (as in the
+// stepping kernels, D-28; mirrored components negated) before the plane's barrier.
+// The z taps come from a per-thread register window of u_i along z, loaded two
+// planes ahead.  The 256 point values of each plane are reduced in a fixed order
+// (warp butterflies, then the 8 warps in order), so the partial of a (plane, tile)
+// depends on nothing but its data: diag_tiles_kernel then sums the tiles of each
+// plane in tile order, and the host sums the planes in global z order, which makes
+// the numbers independent of the slab decomposition.
 template <int M>
 struct DGGeom {
-  static constexpr int XW = 32 + 2 * M;                       // UX row width
+  static constexpr int XW = 32 + 2 * M;                       // X-part row width
   static constexpr int NX = DG_TY * XW, NY = (DG_TY + 2 * M) * 32;
+  static constexpr int N = NX + NY;                           // staged points per plane
+  static constexpr int PER = (N + 255) / 256;                 // per thread
 };
 
-// u_i at a staged (x, y) of plane z, with the mirror sign of u_d when the index
-// went through an odd number of mirrors in direction d
+// u_i at a staged (x, y) of plane z (z window; the mirror signs are the caller's)
 __device__ __forceinline__ void diag_u(const KParams &p, const double *__restrict__ q, int z,
                                        size_t off, double (&u)[3]) {
   const size_t FS = (size_t)p.nx * p.ny;
@@ -78,8 +82,9 @@ template <int M>
 __global__ void __launch_bounds__(256, 2) diag_kernel(const KParams p, const double *__restrict__ q,
                                                       double *__restrict__ tpart, int ntiles) {
   using G = DGGeom<M>;
-  __shared__ double UX[3][G::NX];
-  __shared__ double UY[3][G::NY];
+  // [buffer][rho, m0, m1, m2 -> u0, u1, u2][staged point] (dynamic: above 48 KB)
+  extern __shared__ double DSM[];
+  double(*U)[4][G::N] = reinterpret_cast<double(*)[4][G::N]>(DSM);
   __shared__ double red[3][8];
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
   const int x0 = blockIdx.x * 32, y0 = blockIdx.y * DG_TY;
@@ -90,10 +95,45 @@ __global__ void __launch_bounds__(256, 2) diag_kernel(const KParams p, const dou
   const int nzo = min(DG_Z, p.nz - z0);
   const size_t off = (size_t)min(y, p.ny - 1) * p.nx + min(x, p.nx - 1);
   const size_t FS = (size_t)p.nx * p.ny;
-  // register window of u_i along z at this thread's (x, y)
-  double uz[3][DG_Z + 2 * M];
+  // in-plane offsets of the points this thread stages, and their mirror parities
+  int hoff[G::PER];
+  unsigned char hflip[G::PER];
 #pragma unroll
-  for (int t = 0; t < DG_Z + 2 * M; ++t) {
+  for (int r = 0; r < G::PER; ++r) {
+    const int idx = tid + 256 * r;
+    hoff[r] = 0;
+    hflip[r] = 0;
+    if (idx < G::N) {
+      int fx = 0, fy = 0, gx, gy;
+      if (idx < G::NX) {  // X part: row rr of the tile, column c of the x-extended row
+        const int rr = idx / G::XW, c = idx - rr * G::XW;
+        gx = bmap(x0 - M + c, p.nx, p.sym[0], fx);
+        gy = min(y0 + rr, p.ny - 1);
+      } else {            // Y part: row c of the y-extended tile, column k & 31
+        const int k = idx - G::NX, c = k >> 5;
+        gx = min(x0 + (k & 31), p.nx - 1);
+        gy = bmap(y0 - M + c, p.ny, p.sym[1], fy);
+      }
+      hoff[r] = gy * p.nx + gx;
+      hflip[r] = (unsigned char)(fx | (fy << 1));
+    }
+  }
+  auto stage = [&](int j, int b) {  // raw rho, m_i of plane z0 + j -> buffer b
+    const double *qp = q + qplane(p, z0 + j);
+#pragma unroll
+    for (int r = 0; r < G::PER; ++r) {
+      const int idx = tid + 256 * r;
+      if (idx < G::N) {
+#pragma unroll
+        for (int f = 0; f < 4; ++f) cp_async8(&U[b][f][idx], qp + f * FS + hoff[r]);
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  // register window of u_i along z at this thread's (x, y): uz[i][t] = u_i(z0 - m + t)
+  constexpr int UW = DG_Z + 2 * M, ZA = 2 * M + 2;
+  double uz[3][UW];
+  auto uzload = [&](int t) {
     double u[3] = {0.0, 0.0, 0.0};
     if (t < nzo + 2 * M) {
       int f;
@@ -103,40 +143,35 @@ __global__ void __launch_bounds__(256, 2) diag_kernel(const KParams p, const dou
     }
 #pragma unroll
     for (int i = 0; i < 3; ++i) uz[i][t] = u[i];
-  }
+  };
+#pragma unroll
+  for (int t = 0; t < (ZA < UW ? ZA : UW); ++t) uzload(t);
+  stage(0, 0);
 #pragma unroll
   for (int j = 0; j < DG_Z; ++j) {
     if (j >= nzo) break;
-    const int z = z0 + j;
-    __syncthreads();  // the previous plane's staged values are consumed
-    for (int idx = tid; idx < G::NX + G::NY; idx += 256) {
-      double u[3];
-      int fx = 0, fy = 0;
-      int gx, gy;
-      if (idx < G::NX) {  // UX: row r of the tile, column c of the x-extended row
-        const int r = idx / G::XW, c = idx - r * G::XW;
-        gx = bmap(x0 - M + c, p.nx, p.sym[0], fx);
-        gy = min(y0 + r, p.ny - 1);
-      } else {            // UY: row c of the y-extended tile, column tx
-        const int k = idx - G::NX, c = k >> 5;
-        gx = min(x0 + (k & 31), p.nx - 1);
-        gy = bmap(y0 - M + c, p.ny, p.sym[1], fy);
-      }
-      diag_u(p, q, z, (size_t)gy * p.nx + gx, u);
-      if (fx) u[0] = -u[0];
-      if (fy) u[1] = -u[1];
+    const int z = z0 + j, b = j & 1;
+    if (j + ZA < UW) uzload(j + ZA);
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    // this thread's staged points: u_i = m_i / rho, mirrored components negated
 #pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        if (idx < G::NX) UX[i][idx] = u[i];
-        else UY[i][idx - G::NX] = u[i];
+    for (int r = 0; r < G::PER; ++r) {
+      const int idx = tid + 256 * r;
+      if (idx < G::N) {
+        const double rr = rcp_rho(U[b][0][idx]);
+        const double u0 = U[b][1][idx] * rr, u1 = U[b][2][idx] * rr, u2 = U[b][3][idx] * rr;
+        U[b][1][idx] = (hflip[r] & 1) ? -u0 : u0;
+        U[b][2][idx] = (hflip[r] & 2) ? -u1 : u1;
+        U[b][3][idx] = u2;
       }
     }
-    __syncthreads();
+    __syncthreads();  // plane j converted; every thread is done with plane j - 1's buffer
+    if (j + 1 < nzo) stage(j + 1, b ^ 1);
     double g[3][3];
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
-      const double *rx = &UX[i][ty * G::XW + tx + M];
-      const double *cy = &UY[i][(ty + M) * 32 + tx];
+      const double *rx = &U[b][1 + i][ty * G::XW + tx + M];
+      const double *cy = &U[b][1 + i][G::NX + (ty + M) * 32 + tx];
       double sx = 0.0, sy = 0.0, sz = 0.0;
 #pragma unroll
       for (int k = 1; k <= M; ++k) {
@@ -461,8 +496,12 @@ cudaError_t xypass_launch(const KParams &p, const double *q, double *qout, doubl
 
 template <int M>
 cudaError_t diag_launch(const KParams &p, const double *q, double *tpart, cudaStream_t s) {
+  constexpr int smem = 2 * 4 * DGGeom<M>::N * (int)sizeof(double);
+  static unsigned done = 0;
+  cudaError_t e = ensure_smem_attr(diag_kernel<M>, smem, done);
+  if (e != cudaSuccess) return e;
   const dim3 grid((p.nx + 31) / 32, (p.ny + DG_TY - 1) / DG_TY, (p.nz + DG_Z - 1) / DG_Z);
-  diag_kernel<M><<<grid, dim3(32, DG_TY), 0, s>>>(p, q, tpart, (int)(grid.x * grid.y));
+  diag_kernel<M><<<grid, dim3(32, DG_TY), smem, s>>>(p, q, tpart, (int)(grid.x * grid.y));
   return cudaGetLastError();
 }
 
