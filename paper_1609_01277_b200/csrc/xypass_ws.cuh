@@ -61,6 +61,9 @@ __device__ __forceinline__ void nbar_arrive(int id, int count) {
 #ifndef OSBLI_XY_EXP_NOSTAGE
 #define OSBLI_XY_EXP_NOSTAGE 0
 #endif
+#ifndef OSBLI_XY_TMA_SYM  // A/B knob: TMA staging also with x/y symmetry
+#define OSBLI_XY_TMA_SYM 0
+#endif
 #ifndef OSBLI_XY_EXP_NOFORM
 #define OSBLI_XY_EXP_NOFORM 0
 #endif
@@ -584,7 +587,7 @@ __global__ void __launch_bounds__(XY_CTA, 1)
     // handles with symmetry boundaries in x or y: with their 8-byte staging TMA
     // measured slower there (1.69 vs 1.58 ms at 256^3 o12; the equation variants
     // without symmetry gain 2 %)
-    const bool tma = use_tma && !(SYM && (p.sym[0] | p.sym[1])) && (p.nx % 2) == 0 &&
+    const bool tma = use_tma && !(SYM && !OSBLI_XY_TMA_SYM && (p.sym[0] | p.sym[1])) && (p.nx % 2) == 0 &&
                      !OSBLI_DEBUG_CHECKS && x0 - Gm::XC >= 0 &&
                      x0 - Gm::XC + PX <= p.nx && y0 - M >= 0 && y0 + XY_TY + M <= p.ny;
     uint64_t *bars = reinterpret_cast<uint64_t *>(SM + Gm::OFF_BAR);
