@@ -508,10 +508,12 @@ def main():
     fl = xyflop if dom == "xypass" else zflop
     achieved_tf = fl * per_launch_pts / (avg * 1e-3) / 1e12
     traffic = None
+    fp64_pct = None
     tpath = os.path.join(ROOT, "profiles", "kernel_traffic.json")
     if os.path.exists(tpath):
         tj = json.load(open(tpath)).get(f"{args.config}:{dom}")
         traffic = tj["dram_bytes_per_launch"] if tj else None
+        fp64_pct = tj.get("fp64_pipe_pct") if tj else None
     roof = {
         "kernel": dom, "bound": "alu", "achieved": achieved_tf, "peak": fp64_peak,
         "unit": "TFLOP/s", "frac": achieved_tf / fp64_peak, "traffic": traffic,
@@ -520,6 +522,7 @@ def main():
         "algorithmic_bytes_per_launch": (xyb if dom == "xypass" else zb) / 3 * per_launch_pts,
         "peak_source": f"FP64 = 148 SMs x 64 lanes x 2 flop x {fmax:.0f} MHz (guide unit counts; DESIGN.md §5)",
         "flops_per_point": fl, "avg_launch_ms": avg,
+        "ncu_fp64_pipe_pct": fp64_pct,  # sm__inst_executed_pipe_fp64 (same ncu capture as traffic)
         "flops_model": ("default operator (DESIGN.md §5); the variant's extra terms are not "
                         "counted, so frac is a lower bound") if any(
                             cfg.get(k) for k in ("visc", "cons", "sym")) else "DESIGN.md §5",

@@ -31,6 +31,8 @@ for r in rows[2:]:
         continue
     rd, wr = val(r, "dram__bytes_read.sum"), val(r, "dram__bytes_write.sum")
     tj[f"{config}:{name}"] = {"dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
-                              "duration_ms_under_ncu": val(r, "gpu__time_duration.sum"), "source": note}
+                              "duration_ms_under_ncu": val(r, "gpu__time_duration.sum"),
+                              "fp64_pipe_pct": val(r, "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"),
+                              "source": note}
 json.dump(tj, open(path, "w"), indent=1)
 print(json.dumps({k: v["dram_bytes_per_launch"] for k, v in tj.items() if ":" in k}, indent=1))
