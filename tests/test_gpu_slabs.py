@@ -25,11 +25,13 @@ def osbli():
 @pytest.mark.parametrize("schedule", [0, 1, 2])
 @pytest.mark.parametrize("order,nslabs,shape", [(4, 2, (24, 20, 16)), (4, 3, (24, 20, 17)),
                                                 (12, 2, (20, 18, 24)), (12, 4, (33, 17, 26)),
-                                                (8, 8, (16, 16, 64)), (12, 2, (64, 48, 80))])
+                                                (8, 8, (16, 16, 64)), (12, 2, (64, 48, 80)),
+                                                (12, 3, (96, 64, 48)), (4, 2, (128, 64, 40))])
 def test_loopback_slabs_bitwise_equal_single_domain(osbli, order, nslabs, shape, schedule):
     """The three stage schedules (plain; z-split: interior z-pass, then the two
     face ranges in one launch; xy-split: face xy-pass, then the interior one;
-    DESIGN.md §6) on 2-8 slabs, uneven splits included."""
+    DESIGN.md §6) on 2-8 slabs, uneven splits included.  The wide grids give the
+    xy-pass tiles that stage by TMA and the z-pass TMA boxes through ghost planes."""
     dx = 2 * math.pi / max(shape)
     dt = 2e-3
     Q = perturbed_tgv(*shape, dx=dx, amp=0.02)
@@ -101,15 +103,19 @@ def test_loopback_switch_combinations(osbli, scheme, visc, nslabs, order):
 
 
 @pytest.mark.parametrize("schedule", [0, 1, 2])
-@pytest.mark.parametrize("order,symz,cons", [(4, False, False), (12, False, False),
-                                             (8, True, False), (6, False, True)])
-def test_single_rank_nccl_path_bitwise(osbli, order, symz, cons, schedule):
+@pytest.mark.parametrize("order,symz,cons,shape", [(4, False, False, (24, 20, 26)),
+                                                   (12, False, False, (24, 20, 26)),
+                                                   (8, True, False, (24, 20, 26)),
+                                                   (6, False, True, (24, 20, 26)),
+                                                   (12, False, False, (96, 64, 26)),
+                                                   (8, True, True, (96, 64, 26))])
+def test_single_rank_nccl_path_bitwise(osbli, order, symz, cons, shape, schedule):
     """One rank with an NCCL unique id runs the distributed code path with NCCL:
     its ghost planes come from itself through ncclSend/ncclRecv (or the mirror),
     the z-pass reads ghost planes, the diagnostics go through ncclAllGather.
     The result equals the single-domain run bitwise.  This exercises the NCCL
-    calls of the multi-GPU path on one GPU without ranks waiting on each other."""
-    shape = (24, 20, 26)
+    calls of the multi-GPU path on one GPU without ranks waiting on each other
+    (the 96 x 64 grids: TMA staging through the ghost planes)."""
     dx, dt = 2 * math.pi / 26, 1e-3
     Q = perturbed_tgv(*shape, dx=dx, amp=0.05)
     uid = osbli.nccl_unique_id()

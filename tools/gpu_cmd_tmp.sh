@@ -1,1 +1,1 @@
-timeout 300 python bench.py > gpurun_out/bench_check.json 2> gpurun_out/bench_check.err; echo rc=$? >> gpurun_out/bench_check.err
+timeout 1200 python -m pytest tests/test_gpu_slabs.py -x -q -m gpu > gpurun_out/t_slabs.log 2>&1; echo rc=$? >> gpurun_out/t_slabs.log
