@@ -1,1 +1,4 @@
-timeout 900 python -m pytest tests/test_gpu_tma.py -x -q -m gpu > gpurun_out/t_tma2.log 2>&1; echo rc=$? >> gpurun_out/t_tma2.log
+for rep in 1 2; do for o in 8 12; do
+python tools/quickbench.py 256 $o 30 2 2>&1 | tail -n 1
+OSBLI_LIB=variants/lib_mixbtr.so python tools/quickbench.py 256 $o 30 2 2>&1 | tail -n 1
+done; done > gpurun_out/ab_mixbtr.txt 2>&1
