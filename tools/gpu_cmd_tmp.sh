@@ -1,4 +1,1 @@
-for rep in 1 2; do for o in 8 12; do
-python tools/quickbench.py 256 $o 30 2 2>&1 | tail -n 1
-OSBLI_LIB=variants/lib_mixbtr.so python tools/quickbench.py 256 $o 30 2 2>&1 | tail -n 1
-done; done > gpurun_out/ab_mixbtr.txt 2>&1
+timeout 600 python tools/tgv_history.py gpurun_out/r2z_tgv64_o4_history.csv > gpurun_out/hist.log 2>&1; echo rc=$? >> gpurun_out/hist.log
