@@ -1,1 +1,1 @@
-timeout 600 python tools/tgv_history.py gpurun_out/r2z_tgv64_o4_history.csv > gpurun_out/hist.log 2>&1; echo rc=$? >> gpurun_out/hist.log
+REPS=3 STEPS=30 bash tools/ab_run.sh ab_fu.txt "8 12" cur fu2 fu3
