@@ -39,6 +39,9 @@ FULL = {  # name: (shape, order)
     "96_o12": ((96, 96, 96), 12),
     "96_o8": ((96, 96, 96), 8),
     "128_o4": ((128, 128, 128), 4),
+    # odd m (the staged-column offset of odd orders), TMA interior tiles, a ragged
+    # last z chunk and two z segments per pencil
+    "96x80x72_o10": ((96, 80, 72), 10),
 }
 
 N256, O256, S256 = 256, 12, 3

@@ -1,1 +1,1 @@
-REPS=3 STEPS=30 bash tools/ab_run.sh ab_fu.txt "8 12" cur fu2 fu3
+timeout 1500 python -m pytest tests/test_gpu_production.py -x -q -m gpu > gpurun_out/t_prod.log 2>&1; echo rc=$? >> gpurun_out/t_prod.log
