@@ -45,6 +45,7 @@ FULL = {  # name: (shape, order)
 }
 
 N256, O256, S256 = 256, 12, 3
+O256_ALL = (12, 8)  # BASELINE configs[3] (12th order) and configs[4] (8th order, weak scaling)
 # (lo, size) blocks of the 256^3 grid: x tile edges at multiples of 32, y tile
 # edges at multiples of 16, xy-pass segments of 8 planes, z-pass chunks of 32
 # planes, and the periodic wrap in every direction
@@ -86,7 +87,7 @@ def refs(oracle_lib):
     """Every oracle reference of this module, computed concurrently."""
     from oracle import windowed
     orc = oracle_lib
-    pool = ThreadPoolExecutor(max_workers=max(2, min(len(FULL) + len(BLOCKS), os.cpu_count() or 2)))
+    pool = ThreadPoolExecutor(max_workers=max(2, min(len(FULL) + 2 * len(BLOCKS), os.cpu_count() or 2)))
     out = {}
 
     def full_job(shape, order):
@@ -100,9 +101,11 @@ def refs(oracle_lib):
         out[name] = pool.submit(full_job, shape, order)
     shape = (N256,) * 3
     Q256 = _input(shape)
-    p256 = orc.OracleParams(*shape, O256, _dx(shape), dt=tgv_dt(N256), **TGV_PHYS)
-    for b, (lo, size) in enumerate(BLOCKS):
-        out[("256", b)] = pool.submit(windowed.sample_block, p256, Q256, lo, size, 1, S256)
+    for order in O256_ALL:
+        p256 = orc.OracleParams(*shape, order, _dx(shape), dt=tgv_dt(N256), **TGV_PHYS)
+        for b, (lo, size) in enumerate(BLOCKS):
+            out[("256", order, b)] = pool.submit(windowed.sample_block, p256, Q256, lo, size, 1,
+                                                 S256)
     out["Q256"] = Q256
     yield out
     pool.shutdown(wait=True, cancel_futures=True)
@@ -132,20 +135,22 @@ def test_full_field_10_steps_production_paths(osbli, refs, name):
     s.close()
 
 
-def test_bench_workload_256_o12_blocks(osbli, refs):
-    """BASELINE configs[3] (TGV-shaped 256^3, 12th order) in the bench's launch
-    configuration, 3 RK3 steps, 2560 points in 5 blocks against the oracle;
-    the same 3 steps repeated are bitwise identical; mass is conserved."""
+@pytest.mark.parametrize("order", O256_ALL)
+def test_bench_workload_256_blocks(osbli, refs, order):
+    """BASELINE configs[3] (TGV-shaped 256^3, 12th order) and configs[4] (8th order)
+    in the bench's launch configuration, 3 RK3 steps, 2560 points in 5 blocks
+    against the oracle; the same 3 steps repeated are bitwise identical; mass is
+    conserved."""
     Q = refs["Q256"]
     shape = (N256,) * 3
-    s = osbli.Solver(*shape, O256, _dx(shape), tgv_dt(N256), **TGV_PHYS)
+    s = osbli.Solver(*shape, order, _dx(shape), tgv_dt(N256), **TGV_PHYS)
     s.set_state(Q)
     s.step(S256)
     Qg = s.get_state()
     scale = np.max(np.abs(Qg.reshape(5, -1)), axis=1)
     worst = np.zeros(5)
     for b, (lo, size) in enumerate(BLOCKS):
-        ref = refs[("256", b)].result()
+        ref = refs[("256", order, b)].result()
         ix = [(np.arange(size[d]) + lo[d]) % N256 for d in range(3)]
         got = Qg[:, ix[2]][:, :, ix[1]][:, :, :, ix[0]]
         err = np.max(np.abs(got - ref).reshape(5, -1), axis=1) / scale
