@@ -1,1 +1,1 @@
-timeout 1500 python -m pytest tests/test_gpu_production.py -x -q -m gpu > gpurun_out/t_prod.log 2>&1; echo rc=$? >> gpurun_out/t_prod.log
+timeout 1800 python -m pytest tests -q -m gpu > gpurun_out/t_final2.log 2>&1; echo rc=$? >> gpurun_out/t_final2.log
