@@ -4,15 +4,18 @@ namespace ws {
 // A CTA owns a 32 x 16 tile of the xy-plane and marches through a segment of
 // z-planes (one CTA per SM), warp-specialised:
 //   producers (warps 8-11, setmaxnreg 40): stream plane z+1 into the other plane
-//     buffer with cp.async (periodic wrap or mirror in x, y) and prefetch its
-//     low-storage register W' (= A W + dt Rz from the z-pass) into L2;
+//     buffer -- TMA tensor boxes (one 5-field Q box, g22, g02, g12) completing on
+//     the buffer's mbarrier where the tile's halo does not wrap, a cp.async gather
+//     (periodic wrap or mirror in x, y) elsewhere -- and prefetch its low-storage
+//     register W' (= A W + dt Rz from the z-pass) into L2;
 //   group A (velocity, 4 warps, setmaxnreg 232): p and 1/rho of every staged
 //     point (formulas P:127, EOS P:259-266), velocity gradients, viscous
 //     Laplacians, mixed derivatives (commuted: D-7), dissipation;
 //   group B (conservative, 4 warps): skew-symmetric advection and fluxes
 //     (P:271-274), heat flux, and the stage update of its points,
 //     W <- W' + dt R_xy, Q' <- Q + B W.
-// Per plane, shared memory holds on the tile plus an m-wide halo: rho, m_i, e,
+// Per plane, shared memory holds on the tile plus an m-wide halo (one extra
+// column on each side at odd m): rho, m_i, e,
 // g22 (double-buffered plane buffers), g02 on the tile rows (x-halo), g12 on
 // the tile columns (y-halo); p, 1/rho; g00, g10 extended over the y-halo; the
 // groups' x-partials XA, XB.  u_i = m_i r and T = gamma M^2 p r are formed in
