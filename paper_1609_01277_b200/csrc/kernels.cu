@@ -6,11 +6,12 @@
 //            (D_z, D_zz; P:271-274 skew terms, P:274 Laplacians), written as a
 //            partial residual Rz[5] plus the velocity gradients g_i2 = D_z u_i.
 //            A CTA stages 32 x-columns x (TZ+2m) z-planes of the 13 z-stencil
-//            operands in shared memory (computed once per staged point) and
+//            operands in shared memory (computed once per staged point; the raw
+//            planes arrive by TMA boxes) and
 //            each thread produces RZ = 4 consecutive z outputs from a register
 //            window (reuse (RZ+2m)/RZ instead of 2m loads per output).
 //   xypass : all x/y terms on a 32x16 plane tile with an m-wide halo in
-//            shared memory (warp-specialised: a cp.async producer warpgroup and
+//            shared memory (warp-specialised: a TMA / cp.async producer warpgroup and
 //            two decoupled consumer groups, xypass_ws.cuh), the mixed
 //            derivatives (commuted so that no z stencil is needed:
 //            D_x D_z u_z = D_x g_22, D_z D_x u_x = D_x g_02, ...; D-7),
