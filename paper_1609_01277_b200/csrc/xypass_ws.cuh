@@ -454,18 +454,38 @@ __device__ __forceinline__ void xy_mirror_signs(const KParams &p, double *PB, in
   constexpr int HX = Gm::HX, HY = Gm::HY, PX = Gm::PX, FSZ = Gm::FSZ;
   const bool xs = p.sym[0] && (x0 - Gm::XC < 0 || x0 + XY_TX + Gm::XC > p.nx);
   const bool ys = p.sym[1] && (y0 - M < 0 || y0 + XY_TY + M > p.ny);
-  if (!xs && !ys) return;
+  // only staged columns (rows) outside the grid can come through a mirror: the x
+  // pass visits those columns and fixes rho u_x and g02, the y pass those rows and
+  // fixes rho u_y and g12
+  if (xs) {
+    const int lo = max(0, min(HX, Gm::XC - x0));          // x < 0
+    const int hi = max(lo, min(HX, p.nx - x0 + Gm::XC));  // x >= nx
+    const int nb = lo + (HX - hi);
 #pragma unroll 1
-  for (int idx = tid; idx < HY * HX; idx += nthr) {
-    const int hy = idx / HX, hx = idx - hy * HX;
-    int fx, fy;
-    bmap(x0 - Gm::XC + hx, p.nx, p.sym[0], fx);
-    bmap(y0 - M + hy, p.ny, p.sym[1], fy);
-    double *d = PB + hy * PX + hx;
-    if (fx) d[XF_M0 * FSZ] = -d[XF_M0 * FSZ];
-    if (fy) d[XF_M1 * FSZ] = -d[XF_M1 * FSZ];
-    if (fx && hy >= M && hy < M + XY_TY) PB[Gm::PB_G02 + (hy - M) * PX + hx] *= -1.0;
-    if (fy && hx >= Gm::XC && hx < Gm::XC + XY_TX) PB[Gm::PB_G12 + hy * Gm::GP + hx - Gm::XC] *= -1.0;
+    for (int idx = tid; idx < HY * nb; idx += nthr) {
+      const int hy = idx / nb, k = idx - hy * nb, hx = k < lo ? k : hi + (k - lo);
+      int fx;
+      bmap(x0 - Gm::XC + hx, p.nx, p.sym[0], fx);
+      if (!fx) continue;
+      double *d = PB + hy * PX + hx;
+      d[XF_M0 * FSZ] = -d[XF_M0 * FSZ];
+      if (hy >= M && hy < M + XY_TY) PB[Gm::PB_G02 + (hy - M) * PX + hx] *= -1.0;
+    }
+  }
+  if (ys) {
+    const int lo = max(0, min(HY, M - y0));          // y < 0
+    const int hi = max(lo, min(HY, p.ny - y0 + M));  // y >= ny
+    const int nb = lo + (HY - hi);
+#pragma unroll 1
+    for (int idx = tid; idx < nb * HX; idx += nthr) {
+      const int k = idx / HX, hx = idx - k * HX, hy = k < lo ? k : hi + (k - lo);
+      int fy;
+      bmap(y0 - M + hy, p.ny, p.sym[1], fy);
+      if (!fy) continue;
+      double *d = PB + hy * PX + hx;
+      d[XF_M1 * FSZ] = -d[XF_M1 * FSZ];
+      if (hx >= Gm::XC && hx < Gm::XC + XY_TX) PB[Gm::PB_G12 + hy * Gm::GP + hx - Gm::XC] *= -1.0;
+    }
   }
 }
 
