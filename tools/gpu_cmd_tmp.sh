@@ -1,4 +1,3 @@
-timeout 900 python -m pytest tests/test_gpu_symmetry.py tests/test_gpu_combinations.py tests/test_gpu_variants.py -x -q -m gpu > gpurun_out/t_sym2.log 2>&1; echo rc=$? >> gpurun_out/t_sym2.log
-for rep in 1 2; do for lib in "" variants/lib_base.so; do
+for rep in 1 2; do for lib in "" variants/lib_tmasym.so; do
 OSBLI_LIB=$lib timeout 300 python bench.py --no-cpu-baseline --config tgv256_o12_sym --e2e-steps 1 2>/dev/null | python -c "import json,sys; d=json.load(sys.stdin); r=d['roofline']; print('$lib sym', round(d['value']/1e9,3), round(d['ms_per_step'],3), round(r['avg_launch_ms'],3), round(r['other_kernel']['avg_launch_ms'],3), d['clocks']['sm_mhz'])"
-done; done > gpurun_out/ab_sym2.txt 2>&1
+done; done > gpurun_out/ab_sym3.txt 2>&1
