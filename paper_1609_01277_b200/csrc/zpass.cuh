@@ -9,7 +9,7 @@
 // the xy-pass.
 //
 // A CTA owns a pencil of 32 x-columns x one y-row and marches through its
-// z-range in chunks of TZ = 32 planes.  Shared memory holds a ring of
+// z-range in chunks of TZ = 16 planes (two CTAs per SM).  Shared memory holds a ring of
 // NR = TZ + 2m planes of the 13 z-stencil operands (formulas computed once per
 // plane): consecutive chunks share their 2m overlap planes, so every
 // plane is loaded from HBM once.  While chunk k is computed, the raw state of
@@ -20,8 +20,12 @@
 // thread produces RZ = 4 consecutive z outputs of its column from register
 // windows.
 constexpr int ZP_TX = 32;
+// 16-plane chunks of 4 warps, two CTAs per SM (113.7 KB of shared memory each at
+// m = 6): the ring advance of one CTA (two block barriers) overlaps the other's
+// stencils (round 2: -6 % z-pass at o8, -2..-5 % at o12; 32-plane chunks of 8
+// warps, one CTA per SM, before)
 #ifndef OSBLI_ZP_TZ
-#define OSBLI_ZP_TZ 32
+#define OSBLI_ZP_TZ 16
 #endif
 #ifndef OSBLI_ZP_RZ
 #define OSBLI_ZP_RZ 4
@@ -33,7 +37,7 @@ constexpr int ZP_TX = 32;
 #define OSBLI_ZP_PERSIST 0
 #endif
 #ifndef OSBLI_ZP_MINB
-#define OSBLI_ZP_MINB 1
+#define OSBLI_ZP_MINB 2
 #endif
 constexpr int ZP_TZ = OSBLI_ZP_TZ;  // planes per chunk
 constexpr int ZP_RZ = OSBLI_ZP_RZ;  // z outputs per thread
