@@ -1,3 +1,3 @@
-export OSBLI_LIB=variants/lib_dbg.so
-timeout 1500 python -m pytest tests/test_gpu_production.py tests/test_gpu_parity.py tests/test_gpu_slabs.py tests/test_gpu_variants.py tests/test_gpu_symmetry.py tests/test_gpu_combinations.py -x -q -m gpu > gpurun_out/dbg_t1.log 2>&1; echo rc=$? >> gpurun_out/dbg_t1.log
-OSBLI_NO_SPLIT=1 timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_slabs.py tests/test_gpu_symmetry.py tests/test_gpu_combinations.py -x -q -m gpu > gpurun_out/dbg_t2.log 2>&1; echo rc=$? >> gpurun_out/dbg_t2.log
+for rep in 1 2; do for lib in "" variants/lib_ty8.so variants/lib_ty8z32.so; do
+OSBLI_LIB=$lib timeout 300 python bench.py --no-cpu-baseline --config scalar256_o12 --e2e-steps 1 2>/dev/null | python -c "import json,sys; d=json.load(sys.stdin); print('$lib', d['value']/1e9, d['ms_per_step'])"
+done; done > gpurun_out/ab_sc_ty.txt 2>&1
